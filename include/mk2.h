@@ -1,0 +1,165 @@
+/*
+ * mk2.h -- C ABI of the B200-native bitsliced MICKEY 2.0 keystream generator.
+ *
+ * This is the drop-in boundary for ONE path of the reference package
+ * `slicerng` (arxiv 1909.04750): bulk MICKEY 2.0 keystream generation.  The
+ * reference is pure Python + numba and has no FFI of its own; each entry point
+ * below names the reference function (path:line under /root/reference/) whose
+ * work it replaces, and INTEGRATION.md shows the ctypes binding a maintainer of
+ * the reference would add.  Plain pointers and sizes only; no exceptions, no
+ * C++/torch types.  Every function returns 0 on success or a negative
+ * MK2_E* code; mk2_last_error() gives the text.  There is NO CPU fallback:
+ * without an sm_100 device mk2_create() fails.
+ *
+ * Geometry: N instances are processed as G = ceil(N/32) groups; one GPU thread
+ * owns one group (32 instances, column-major: one 32-bit word per bit of the
+ * 100-bit R and S registers -- MickeySliced, pkg/src/slicerng/mickey.py:236).
+ * Pointers marked "host or device" are classified with
+ * cudaPointerGetAttributes; device pointers are used in place (e.g. a torch
+ * CUDA tensor's data_ptr()), host pointers are staged through pinned buffers.
+ *
+ * Threading: a context is exclusively owned by one thread at a time
+ * (SPEC.md:336-337 gives the reference's engines the same rule); use one
+ * context per (thread, device).
+ */
+#ifndef MK2_H
+#define MK2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mk2_ctx mk2_ctx;
+
+enum {
+    MK2_OK = 0,
+    MK2_E_CUDA = -1,     /* a CUDA runtime call failed (text in mk2_last_error) */
+    MK2_E_ARG = -2,      /* invalid argument */
+    MK2_E_STATE = -3,    /* context not initialised with key/IV material yet */
+    MK2_E_NODEVICE = -4, /* no CUDA device / not an sm_100 part */
+    MK2_E_NOMEM = -5
+};
+
+#define MK2_IV_UNUSED 0xFFu /* mk2_init_ragged: lane stays in the all-zero state */
+
+/* Library / device discovery. */
+int mk2_abi_version(void); /* currently 1 */
+int mk2_device_count(void);
+
+/* Context = one device, one stream, the state of N instances. */
+int mk2_create(int device, mk2_ctx **out);
+int mk2_destroy(mk2_ctx *ctx);
+/* Launch on the caller's stream (e.g. torch's current stream) instead of the
+ * context's own; pass NULL to go back to the private stream. */
+int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream);
+int mk2_sync(mk2_ctx *ctx);
+const char *mk2_last_error(const mk2_ctx *ctx); /* ctx may be NULL: last create error */
+
+/* Shard bookkeeping: this context holds global groups
+ * [group_offset, group_offset + G).  Only the checksum weighting uses it. */
+int mk2_set_group_offset(mk2_ctx *ctx, uint64_t group_offset);
+
+/*
+ * Key/IV load + 100 pre-clocks for N instances with one common IV bit length.
+ * Replaces MickeySliced.from_key_ivs, uniform route
+ * (pkg/src/slicerng/mickey.py:258-304, word-wide load :291-303).
+ *   keys: N x 10 bytes, row-major, bit k_0 = MSB of byte 0 (bitops.py:33-36)
+ *   ivs : N rows of iv_stride bytes (>= ceil(iv_bits/8)), MSB-first; may be
+ *         NULL when iv_bits == 0
+ *   iv_bits: 0..80
+ * keys / ivs: host or device.  Lanes N..32*G-1 load zero material, like the
+ * reference's unused lanes.
+ */
+int mk2_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
+                           uint32_t iv_bits, uint64_t N);
+
+/*
+ * Same with a per-instance IV bit length (the reference's ragged route,
+ * mickey.py:287-289 + from_scalar_states :306-316).  iv_nbits[n] in 0..80, or
+ * MK2_IV_UNUSED for a lane that must stay in the all-zero state.
+ */
+int mk2_init_ragged(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
+                    const uint8_t *iv_nbits, uint64_t N);
+
+/*
+ * Synthetic material generated on the device: every instance
+ * uses `key`; instance n gets the 80-bit big-endian IV (first_index + n).
+ * first_index must be a multiple of 32.  No host->device traffic.
+ */
+int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_index, uint64_t N);
+
+/*
+ * T more keystream clocks, column-major ("bit-interleaved",
+ * docs/conventions.md:61-63): out[t * stride_words + g] is a uint32 whose bit j
+ * is keystream bit t of instance 32 g + j.  For N = 64 and stride 2 the buffer
+ * is byte-identical to the uint64 array kernels.mickey_sliced_words returns
+ * (pkg/src/slicerng/kernels.py:189-200).  Replaces the compiled loop
+ * kernels._mickey_sliced_loop (kernels.py:46-95) and
+ * MickeySliced.keystream_words (mickey.py:362-368); resumable like the latter.
+ * out: host or device; stride_words >= G.
+ */
+int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words);
+
+/*
+ * T more keystream clocks (T % 8 == 0, bitops.py:17-18), row-major
+ * ("lane-major", docs/conventions.md:58-60): row n = instance n, T/8 bytes,
+ * first bit in the MSB of the first byte -- what kernels.words_to_lane_bytes /
+ * words_lane_major_bytes (kernels.py:604-621) produce from the words.
+ * out points at the first NEW byte of row 0; pitch_bytes is the row stride, so
+ * successive calls can fill a longer row chunk by chunk.  out: host or device.
+ */
+int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes);
+
+/*
+ * n raw CLOCK_KG steps without output: MickeySliced.clock_kg(mixing, word)
+ * (pkg/src/slicerng/mickey.py:329-360).  input_words: uint32 [n][G] (bit j of
+ * word [c][g] = input bit of instance 32 g + j at step c) or NULL for zero
+ * input.  host or device.  Not a throughput path.
+ */
+int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n);
+
+/* Number of instances / groups / clocks emitted since init. */
+int mk2_query(const mk2_ctx *ctx, uint64_t *N, uint64_t *G, uint64_t *clocks);
+
+/*
+ * Raw sliced state, uint32 rs[200][G]: rs[i][g] = R bit i, rs[100+i][g] = S
+ * bit i of group g (MickeySliced.rregs/.sregs, mickey.py:250-251).  Import
+ * also (re)sizes the context to N instances and clears the checksum.
+ * rs: host or device.
+ */
+int mk2_state_export(mk2_ctx *ctx, uint32_t *rs);
+int mk2_state_import(mk2_ctx *ctx, const uint32_t *rs, uint64_t N);
+
+/*
+ * Checksum of everything emitted since init: the column-major stream read as
+ * little-endian uint64 words (group g + group_offset even = low half) and
+ * summed mod 2^64.  Layout independent; additive over disjoint group ranges,
+ * so per-GPU values can be combined with one 8-byte ncclSum all-reduce.
+ */
+int mk2_checksum(mk2_ctx *ctx, uint64_t *sum);
+
+/* Device time (ms, CUDA events on the launch stream) of the kernels launched by
+ * the most recent init / generate call, and how many kernels that was. */
+float mk2_last_kernel_ms(const mk2_ctx *ctx);
+int mk2_last_kernel_launches(const mk2_ctx *ctx);
+/* Skip the per-call event synchronisation (for callers that time the stream
+ * themselves); mk2_last_kernel_ms is then only valid after mk2_sync. */
+int mk2_set_async(mk2_ctx *ctx, int async);
+
+/*
+ * Roofline probe: sustained LOP3 lane-operations per second of this device,
+ * measured with a dependency-free LOP3 kernel.
+ */
+int mk2_lop3_peak(mk2_ctx *ctx, double *lane_ops_per_s, float *ms);
+
+/* Static facts about the kernels (for DESIGN.md / bench.py): ALU-pipe logic ops
+ * per keystream clock per 32-lane word as counted in SURVEY.md 8(d). */
+int mk2_lop3_per_clock(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MK2_H */

@@ -1,0 +1,602 @@
+// mk2_api.cu -- C-ABI shim (include/mk2.h) over the sm_100a kernels.
+// Host side only does pointer classification, chunking and launches; all
+// cipher work is in mk2_kernels.cuh.  No CPU fallback exists in this file.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/mk2.h"
+#include "mk2_kernels.cuh"
+
+using namespace mk2;
+
+namespace {
+std::string g_create_error;
+constexpr size_t STAGE_BYTES = size_t(256) << 20;  // per staging buffer for host outputs
+}  // namespace
+
+struct mk2_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own = nullptr, stream = nullptr, copy = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t gen_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+    bool copy_pending[2] = {false, false};
+    uint64_t N = 0, G = 0, cap = 0, g_offset = 0, clocks = 0;
+    uint32_t *d_state = nullptr;
+    unsigned long long *d_acc = nullptr, *d_sum = nullptr;
+    void *d_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    bool ready = false, async = false, timing_open = false;
+    float last_ms = 0.f;
+    int last_launches = 0;
+    std::string err;
+};
+
+namespace {
+
+int fail(mk2_ctx *c, int code, const std::string &msg)
+{
+    if (c) c->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? MK2_E_NOMEM : MK2_E_CUDA,            \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+    } while (0)
+
+bool is_device_ptr(const void *p)
+{
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+inline unsigned blocks_for(uint64_t G) { return (unsigned)((G + BLOCK - 1) / BLOCK); }
+
+int begin_timing(mk2_ctx *ctx)
+{
+    ctx->last_launches = 0;
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    return MK2_OK;
+}
+
+int end_timing(mk2_ctx *ctx)
+{
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->timing_open = true;
+    if (!ctx->async) {
+        CK(cudaEventSynchronize(ctx->ev1));
+        CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+        ctx->timing_open = false;
+    }
+    return MK2_OK;
+}
+
+int ensure_capacity(mk2_ctx *ctx, uint64_t G)
+{
+    if (G <= ctx->cap) return MK2_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->d_state) cudaFree(ctx->d_state);
+    if (ctx->d_acc) cudaFree(ctx->d_acc);
+    ctx->d_state = nullptr;
+    ctx->d_acc = nullptr;
+    ctx->cap = 0;
+    CK(cudaMalloc(&ctx->d_state, sizeof(uint32_t) * 2 * NBITS * G));
+    CK(cudaMalloc(&ctx->d_acc, sizeof(unsigned long long) * G));
+    ctx->cap = G;
+    return MK2_OK;
+}
+
+int ensure_stage(mk2_ctx *ctx, size_t bytes)
+{
+    if (bytes <= ctx->stage_bytes) return MK2_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->copy));
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->d_stage[b]) cudaFree(ctx->d_stage[b]);
+        ctx->d_stage[b] = nullptr;
+        ctx->copy_pending[b] = false;
+    }
+    ctx->stage_bytes = 0;
+    for (int b = 0; b < 2; ++b) CK(cudaMalloc(&ctx->d_stage[b], bytes));
+    ctx->stage_bytes = bytes;
+    return MK2_OK;
+}
+
+// Bring a host-or-device input array onto the device (stream ordered).
+int stage_input(mk2_ctx *ctx, const void *src, size_t bytes, const uint8_t **dev, void **owned)
+{
+    *owned = nullptr;
+    if (bytes == 0 || src == nullptr) {
+        *dev = nullptr;
+        return MK2_OK;
+    }
+    if (is_device_ptr(src)) {
+        *dev = static_cast<const uint8_t *>(src);
+        return MK2_OK;
+    }
+    CK(cudaMallocAsync(owned, bytes, ctx->stream));
+    CK(cudaMemcpyAsync(*owned, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *dev = static_cast<const uint8_t *>(*owned);
+    return MK2_OK;
+}
+
+int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bool ragged)
+{
+    const unsigned nb = blocks_for(ctx->G);
+    if (ragged)
+        init_kernel<true><<<nb, BLOCK, 0, ctx->stream>>>(mat, load_clocks, lmax, ctx->G, ctx->d_state, ctx->d_acc);
+    else
+        init_kernel<false><<<nb, BLOCK, 0, ctx->stream>>>(mat, load_clocks, lmax, ctx->G, ctx->d_state, ctx->d_acc);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    ctx->clocks = 0;
+    ctx->ready = true;
+    return MK2_OK;
+}
+
+int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
+{
+    gen_colmajor_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, stride,
+                                                                       ctx->G, T);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    return MK2_OK;
+}
+
+int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch)
+{
+    const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
+    if (aligned)
+        gen_rowmajor_kernel<true><<<blocks_for(ctx->G), BLOCK, ROW_SMEM_BYTES, ctx->stream>>>(
+            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T);
+    else
+        gen_rowmajor_kernel<false><<<blocks_for(ctx->G), BLOCK, ROW_SMEM_BYTES, ctx->stream>>>(
+            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    return MK2_OK;
+}
+
+// host-output helper: make staging buffer b safe to overwrite
+int acquire_stage(mk2_ctx *ctx, int b)
+{
+    if (ctx->copy_pending[b]) {
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->copy_done[b], 0));
+        ctx->copy_pending[b] = false;
+    }
+    return MK2_OK;
+}
+
+int drain_copies(mk2_ctx *ctx)
+{
+    CK(cudaStreamSynchronize(ctx->copy));
+    ctx->copy_pending[0] = ctx->copy_pending[1] = false;
+    return MK2_OK;
+}
+
+int check_ready(mk2_ctx *ctx)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MK2_E_CUDA, "cudaSetDevice failed");
+    if (!ctx->ready) return fail(ctx, MK2_E_STATE, "context holds no key/IV material: call mk2_init_* first");
+    return MK2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mk2_abi_version(void) { return 1; }
+
+int mk2_lop3_per_clock(void) { return 327; }
+
+int mk2_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int mk2_create(int device, mk2_ctx **out)
+{
+    mk2_ctx *ctx = nullptr;  // CK() reports into g_create_error while ctx == nullptr
+    if (!out) return fail(nullptr, MK2_E_ARG, "out is NULL");
+    *out = nullptr;
+    int n = mk2_device_count();
+    if (n <= 0) return fail(nullptr, MK2_E_NODEVICE, "no CUDA device visible; this library has no CPU fallback");
+    if (device < 0 || device >= n) return fail(nullptr, MK2_E_ARG, "device index out of range");
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(nullptr, MK2_E_NODEVICE,
+                    std::string("device is sm_") + std::to_string(prop.major) + std::to_string(prop.minor) +
+                        "; the kernels are built for sm_100a only");
+    CK(cudaSetDevice(device));
+    mk2_ctx *c = new (std::nothrow) mk2_ctx();
+    if (!c) return fail(nullptr, MK2_E_NOMEM, "out of host memory");
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&c->gen_done[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_done[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_sum, sizeof(unsigned long long));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gen_rowmajor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM_BYTES);
+    if (e != cudaSuccess) {
+        std::string msg = std::string("context setup: ") + cudaGetErrorString(e);
+        mk2_destroy(c);
+        return fail(nullptr, MK2_E_CUDA, msg);
+    }
+    c->stream = c->own;
+    *out = c;
+    return MK2_OK;
+}
+
+int mk2_destroy(mk2_ctx *ctx)
+{
+    if (!ctx) return MK2_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy) cudaStreamSynchronize(ctx->copy);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->d_stage[b]) cudaFree(ctx->d_stage[b]);
+        if (ctx->gen_done[b]) cudaEventDestroy(ctx->gen_done[b]);
+        if (ctx->copy_done[b]) cudaEventDestroy(ctx->copy_done[b]);
+    }
+    if (ctx->d_state) cudaFree(ctx->d_state);
+    if (ctx->d_acc) cudaFree(ctx->d_acc);
+    if (ctx->d_sum) cudaFree(ctx->d_sum);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    delete ctx;
+    return MK2_OK;
+}
+
+int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream)
+{
+    if (!ctx) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own;
+    return MK2_OK;
+}
+
+int mk2_set_async(mk2_ctx *ctx, int async)
+{
+    if (!ctx) return MK2_E_ARG;
+    ctx->async = async != 0;
+    return MK2_OK;
+}
+
+int mk2_sync(mk2_ctx *ctx)
+{
+    if (!ctx) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->copy));
+    if (ctx->timing_open) {
+        CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+        ctx->timing_open = false;
+    }
+    return MK2_OK;
+}
+
+const char *mk2_last_error(const mk2_ctx *ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+int mk2_set_group_offset(mk2_ctx *ctx, uint64_t group_offset)
+{
+    if (!ctx) return MK2_E_ARG;
+    ctx->g_offset = group_offset;
+    return MK2_OK;
+}
+
+int mk2_query(const mk2_ctx *ctx, uint64_t *N, uint64_t *G, uint64_t *clocks)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (N) *N = ctx->N;
+    if (G) *G = ctx->G;
+    if (clocks) *clocks = ctx->clocks;
+    return MK2_OK;
+}
+
+float mk2_last_kernel_ms(const mk2_ctx *ctx) { return ctx ? ctx->last_ms : -1.f; }
+int mk2_last_kernel_launches(const mk2_ctx *ctx) { return ctx ? ctx->last_launches : 0; }
+
+static int init_common(mk2_ctx *ctx, uint64_t N)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (N == 0) return fail(ctx, MK2_E_ARG, "at least one lane is required");
+    CK(cudaSetDevice(ctx->device));
+    const uint64_t G = (N + 31) / 32;
+    int rc = ensure_capacity(ctx, G);
+    if (rc) return rc;
+    ctx->N = N;
+    ctx->G = G;
+    ctx->ready = false;
+    return MK2_OK;
+}
+
+int mk2_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
+                           uint32_t iv_bits, uint64_t N)
+{
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
+    if (!keys) return fail(ctx, MK2_E_ARG, "keys is NULL");
+    if (iv_bits > 80) return fail(ctx, MK2_E_ARG, "IV must be at most 80 bits");
+    if (iv_bits && (!ivs || iv_stride < (iv_bits + 7) / 8)) return fail(ctx, MK2_E_ARG, "ivs/iv_stride too small for iv_bits");
+    if ((rc = begin_timing(ctx))) return rc;
+    const uint8_t *dk = nullptr, *di = nullptr;
+    void *ok = nullptr, *oi = nullptr;
+    uint32_t *mat = nullptr;
+    if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
+    if ((rc = stage_input(ctx, iv_bits ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
+    const int load = (int)iv_bits + KEY_BITS;
+    CK(cudaMallocAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->stream));
+    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, N, ctx->G, mat);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    if ((rc = launch_init(ctx, mat, load, 0, false))) return rc;
+    CK(cudaFreeAsync(mat, ctx->stream));
+    if (ok) CK(cudaFreeAsync(ok, ctx->stream));
+    if (oi) CK(cudaFreeAsync(oi, ctx->stream));
+    return end_timing(ctx);
+}
+
+int mk2_init_ragged(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
+                    const uint8_t *iv_nbits, uint64_t N)
+{
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
+    if (!keys || !iv_nbits) return fail(ctx, MK2_E_ARG, "keys / iv_nbits is NULL");
+    // the lengths steer the launch, so they are needed on the host
+    std::string lens(N, '\0');
+    if (is_device_ptr(iv_nbits)) {
+        CK(cudaMemcpyAsync(&lens[0], iv_nbits, N, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+        std::memcpy(&lens[0], iv_nbits, N);
+    }
+    int lmax = 0;
+    for (uint64_t n = 0; n < N; ++n) {
+        const unsigned l = (unsigned char)lens[n];
+        if (l == MK2_IV_UNUSED) continue;
+        if (l > 80) return fail(ctx, MK2_E_ARG, "lane " + std::to_string(n) + ": IV must be at most 80 bits");
+        lmax = std::max(lmax, (int)l);
+    }
+    if (lmax && (!ivs || iv_stride < (uint32_t)(lmax + 7) / 8)) return fail(ctx, MK2_E_ARG, "ivs/iv_stride too small");
+    if ((rc = begin_timing(ctx))) return rc;
+    const uint8_t *dk = nullptr, *di = nullptr, *dn = nullptr;
+    void *ok = nullptr, *oi = nullptr, *on = nullptr;
+    uint32_t *mat = nullptr;
+    if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
+    if ((rc = stage_input(ctx, lmax ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
+    if ((rc = stage_input(ctx, iv_nbits, N, &dn, &on))) return rc;
+    const int load = lmax + KEY_BITS;
+    CK(cudaMallocAsync(&mat, sizeof(uint32_t) * (size_t)(2 * lmax + KEY_BITS + 1) * ctx->G, ctx->stream));
+    pack_ragged_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, dn, lmax, N, ctx->G, mat);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    if ((rc = launch_init(ctx, mat, load, lmax, true))) return rc;
+    CK(cudaFreeAsync(mat, ctx->stream));
+    if (ok) CK(cudaFreeAsync(ok, ctx->stream));
+    if (oi) CK(cudaFreeAsync(oi, ctx->stream));
+    if (on) CK(cudaFreeAsync(on, ctx->stream));
+    return end_timing(ctx);
+}
+
+int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_index, uint64_t N)
+{
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
+    if (!key) return fail(ctx, MK2_E_ARG, "key is NULL");
+    if (first_index % 32) return fail(ctx, MK2_E_ARG, "first_index must be a multiple of 32");
+    if (first_index + N < first_index) return fail(ctx, MK2_E_ARG, "instance index range overflows 64 bits");
+    uint64_t hi = ((uint64_t)key[0] << 8) | key[1], lo = 0;
+    for (int i = 2; i < 10; ++i) lo = (lo << 8) | key[i];
+    if ((rc = begin_timing(ctx))) return rc;
+    uint32_t *mat = nullptr;
+    CK(cudaMallocAsync(&mat, sizeof(uint32_t) * (size_t)160 * ctx->G, ctx->stream));
+    pack_counter_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(hi, lo, first_index, ctx->G, mat);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    if ((rc = launch_init(ctx, mat, 160, 0, false))) return rc;
+    CK(cudaFreeAsync(mat, ctx->stream));
+    return end_timing(ctx);
+}
+
+int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words)
+{
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    if (T == 0) {  // zero-length request leaves the state untouched (tests/test_mickey.py:167-171)
+        ctx->last_ms = 0.f;
+        ctx->last_launches = 0;
+        return MK2_OK;
+    }
+    if (!out) return fail(ctx, MK2_E_ARG, "out is NULL");
+    if (stride_words < ctx->G) return fail(ctx, MK2_E_ARG, "stride_words smaller than the group count");
+    if (reinterpret_cast<uintptr_t>(out) % 4) return fail(ctx, MK2_E_ARG, "out must be 4-byte aligned");
+    if ((rc = begin_timing(ctx))) return rc;
+    if (is_device_ptr(out)) {
+        if ((rc = launch_col(ctx, T, static_cast<uint32_t *>(out), stride_words))) return rc;
+    } else {
+        const size_t row_bytes = ctx->G * sizeof(uint32_t);
+        const size_t want = std::max<size_t>(std::min<size_t>(STAGE_BYTES, T * row_bytes), row_bytes);
+        if ((rc = ensure_stage(ctx, want))) return rc;
+        const uint64_t chunk = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
+        int b = 0;
+        for (uint64_t t0 = 0; t0 < T; t0 += chunk, b ^= 1) {
+            const uint64_t tc = std::min(chunk, T - t0);
+            if ((rc = acquire_stage(ctx, b))) return rc;
+            if ((rc = launch_col(ctx, tc, static_cast<uint32_t *>(ctx->d_stage[b]), ctx->G))) return rc;
+            CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
+            uint8_t *dst = static_cast<uint8_t *>(out) + t0 * stride_words * sizeof(uint32_t);
+            CK(cudaMemcpy2DAsync(dst, stride_words * sizeof(uint32_t), ctx->d_stage[b], row_bytes, row_bytes, tc,
+                                 cudaMemcpyDeviceToHost, ctx->copy));
+            CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
+            ctx->copy_pending[b] = true;
+        }
+        if ((rc = drain_copies(ctx))) return rc;
+    }
+    ctx->clocks += T;
+    return end_timing(ctx);
+}
+
+int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes)
+{
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    if (T % 8) return fail(ctx, MK2_E_ARG, "bit count must be a multiple of 8");
+    if (T == 0) {
+        ctx->last_ms = 0.f;
+        ctx->last_launches = 0;
+        return MK2_OK;
+    }
+    if (!out) return fail(ctx, MK2_E_ARG, "out is NULL");
+    if (pitch_bytes < T / 8) return fail(ctx, MK2_E_ARG, "pitch_bytes smaller than T/8");
+    if ((rc = begin_timing(ctx))) return rc;
+    if (is_device_ptr(out)) {
+        if ((rc = launch_row(ctx, T, static_cast<uint8_t *>(out), pitch_bytes))) return rc;
+    } else {
+        // stage [N][tc/8] tiles; tc a multiple of 128 clocks keeps the 16-byte store path
+        const uint64_t min_bytes = ctx->N * 16;
+        const size_t want = std::max<size_t>(std::min<size_t>(STAGE_BYTES, ctx->N * ((T + 127) / 128 * 16)), min_bytes);
+        if ((rc = ensure_stage(ctx, want))) return rc;
+        const uint64_t chunk = std::max<uint64_t>(128, ctx->stage_bytes / ctx->N / 16 * 128);
+        int b = 0;
+        for (uint64_t t0 = 0; t0 < T; t0 += chunk, b ^= 1) {
+            const uint64_t tc = std::min(chunk, T - t0);
+            const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
+            if ((rc = acquire_stage(ctx, b))) return rc;
+            if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp))) return rc;
+            CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
+            uint8_t *dst = static_cast<uint8_t *>(out) + t0 / 8;
+            CK(cudaMemcpy2DAsync(dst, pitch_bytes, ctx->d_stage[b], sp, tc / 8, ctx->N, cudaMemcpyDeviceToHost,
+                                 ctx->copy));
+            CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
+            ctx->copy_pending[b] = true;
+        }
+        if ((rc = drain_copies(ctx))) return rc;
+    }
+    ctx->clocks += T;
+    return end_timing(ctx);
+}
+
+int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n)
+{
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    if (n == 0) return MK2_OK;
+    if ((rc = begin_timing(ctx))) return rc;
+    const uint8_t *din = nullptr;
+    void *owned = nullptr;
+    if ((rc = stage_input(ctx, input_words, input_words ? sizeof(uint32_t) * n * ctx->G : 0, &din, &owned))) return rc;
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(din);
+    if (mixing)
+        clock_kernel<true><<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
+    else
+        clock_kernel<false><<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    if (owned) CK(cudaFreeAsync(owned, ctx->stream));
+    return end_timing(ctx);
+}
+
+int mk2_state_export(mk2_ctx *ctx, uint32_t *rs)
+{
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    if (!rs) return fail(ctx, MK2_E_ARG, "rs is NULL");
+    const size_t bytes = sizeof(uint32_t) * 2 * NBITS * ctx->G;
+    CK(cudaMemcpyAsync(rs, ctx->d_state, bytes, is_device_ptr(rs) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return MK2_OK;
+}
+
+int mk2_state_import(mk2_ctx *ctx, const uint32_t *rs, uint64_t N)
+{
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
+    if (!rs) return fail(ctx, MK2_E_ARG, "rs is NULL");
+    const size_t bytes = sizeof(uint32_t) * 2 * NBITS * ctx->G;
+    CK(cudaMemcpyAsync(ctx->d_state, rs, bytes, is_device_ptr(rs) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_acc, 0, sizeof(unsigned long long) * ctx->G, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->clocks = 0;
+    ctx->ready = true;
+    return MK2_OK;
+}
+
+int mk2_checksum(mk2_ctx *ctx, uint64_t *sum)
+{
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    if (!sum) return fail(ctx, MK2_E_ARG, "sum is NULL");
+    CK(cudaMemsetAsync(ctx->d_sum, 0, sizeof(unsigned long long), ctx->stream));
+    const unsigned nb = std::min<unsigned>(blocks_for(ctx->G), 4u * (unsigned)ctx->sm_count);
+    checksum_kernel<<<nb, BLOCK, 0, ctx->stream>>>(ctx->d_acc, ctx->G, ctx->g_offset, ctx->d_sum);
+    CK(cudaGetLastError());
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, ctx->d_sum, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *sum = v;
+    return MK2_OK;
+}
+
+int mk2_lop3_peak(mk2_ctx *ctx, double *lane_ops_per_s, float *ms_out)
+{
+    if (!ctx || !lane_ops_per_s) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    uint32_t *sink = nullptr;
+    const unsigned nb = 8u * (unsigned)ctx->sm_count;
+    CK(cudaMalloc(&sink, sizeof(uint32_t) * nb * BLOCK));
+    const int iters = 2048;
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {  // first repetition is the warm-up
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        lop3_peak_kernel<<<nb, BLOCK, 0, ctx->stream>>>(sink, 12345u + rep, iters);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        if (rep > 0) best = std::min(best, ms);
+    }
+    CK(cudaFree(sink));
+    const double ops = (double)nb * BLOCK * 32.0 / 32.0 * (double)iters * 16.0 * PEAK_UNROLL;
+    *lane_ops_per_s = ops / (best * 1e-3);
+    if (ms_out) *ms_out = best;
+    return MK2_OK;
+}
+
+}  // extern "C"

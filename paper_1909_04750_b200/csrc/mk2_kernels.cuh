@@ -1,0 +1,437 @@
+// mk2_kernels.cuh -- sm_100a kernels of the bitsliced MICKEY 2.0 path.
+//
+// Data layout in HBM (all little-endian uint32 words, G = N/32 groups):
+//   state[200][G]   word i   (i < 100)  = R bit i of the 32 instances of group g
+//                   word 100+i          = S bit i            (mickey.py:236-243)
+//   mat[c][G]       input word of load clock c (bit j = instance j's IV/key bit,
+//                   mickey.py:291-301); ragged sets append activity masks
+//   acc[G]          per-group uint64 sum of every keystream word emitted
+//   out (column)    uint32 out[t][stride]  bit j of out[t][g] = z_t of inst 32g+j
+//   out (row)       uint8  out[n][pitch]   MSB-first bytes   (kernels.py:604-621)
+// Consecutive threads own consecutive groups g, so every access to state / mat /
+// column-major output is a fully coalesced 128-byte warp transaction.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "mk2_clock.cuh"
+
+namespace mk2 {
+
+constexpr int BLOCK = 256;           // 8 warps = 2 per SM sub-partition at 255 regs/thread
+constexpr int ROW_GROUPS = 16;       // 8-clock groups staged per drain = 16 bytes per instance row
+constexpr int ROW_SMEM_BYTES = 8 * ROW_GROUPS * BLOCK * 4;  // 128 KiB
+
+// ---------------------------------------------------------------------------
+// 8 x 32 bit-matrix transpose, in place: afterwards bit (8q + k) of w[b] is the
+// old bit (8q + b) of w[k]  (four independent 8x8 transposes, one per byte
+// column).  Three half-block swap stages, the log-step scheme of the
+// reference's _square_transpose (pkg/src/slicerng/bitslab.py:183-200)
+// restricted to the last three stages.  2 shifts + 2 LOP3 per pair.
+// ---------------------------------------------------------------------------
+template <int S, uint32_t M>
+__device__ __forceinline__ void swap_stage(uint32_t &a, uint32_t &b)
+{
+    const uint32_t na = (a & M) | ((b << S) & ~M);
+    const uint32_t nb = ((a >> S) & M) | (b & ~M);
+    a = na;
+    b = nb;
+}
+__device__ __forceinline__ void transpose8x32(uint32_t (&w)[8])
+{
+    swap_stage<4, 0x0F0F0F0Fu>(w[0], w[4]);
+    swap_stage<4, 0x0F0F0F0Fu>(w[1], w[5]);
+    swap_stage<4, 0x0F0F0F0Fu>(w[2], w[6]);
+    swap_stage<4, 0x0F0F0F0Fu>(w[3], w[7]);
+    swap_stage<2, 0x33333333u>(w[0], w[2]);
+    swap_stage<2, 0x33333333u>(w[1], w[3]);
+    swap_stage<2, 0x33333333u>(w[4], w[6]);
+    swap_stage<2, 0x33333333u>(w[5], w[7]);
+    swap_stage<1, 0x55555555u>(w[0], w[1]);
+    swap_stage<1, 0x55555555u>(w[2], w[3]);
+    swap_stage<1, 0x55555555u>(w[4], w[5]);
+    swap_stage<1, 0x55555555u>(w[6], w[7]);
+}
+
+// ---------------------------------------------------------------------------
+// Material packing: row-major key/IV bytes -> one bitsliced input word per load
+// clock (the word-wide load of mickey.py:291-301, for 32 lanes per thread).
+// nbytes byte columns of `src` (row stride `stride`) become clocks
+// c0 .. c0 + nbits - 1, MSB-first per byte (bitops.py:33-36).  Rows >= N read
+// as zero: the reference's unused lanes (zero material).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pack_bytes_to_clocks(const uint8_t *__restrict__ src, uint32_t stride,
+                                                     uint64_t first_row, uint64_t N, int nbits,
+                                                     uint32_t *__restrict__ mat, uint64_t G, uint64_t g, int c0)
+{
+    const int nbytes = (nbits + 7) >> 3;
+    for (int b = 0; b < nbytes; ++b) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t row = first_row + 8 * q + k;
+                const uint32_t byte = row < N ? src[row * stride + b] : 0u;
+                v |= byte << (8 * q);
+            }
+            w[k] = v;
+        }
+        transpose8x32(w);  // w[bit] = bit `bit` of byte b across the 32 instances
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int c = 8 * b + m;  // clock within this field; bit 7-m of the byte
+            if (c < nbits) mat[(uint64_t)(c0 + c) * G + g] = w[7 - m];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+pack_uniform_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__ ivs, uint32_t iv_stride,
+                    int iv_bits, uint64_t N, uint64_t G, uint32_t *__restrict__ mat)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    pack_bytes_to_clocks(ivs, iv_stride, 32 * g, N, iv_bits, mat, G, g, 0);
+    pack_bytes_to_clocks(keys, 10, 32 * g, N, KEY_BITS, mat, G, g, iv_bits);
+}
+
+// Ragged IV lengths (mickey.py:287-289 falls back to per-lane scalar init; here
+// the lanes stay bitsliced): lane j with L_j IV bits idles in the all-zero
+// state for Lmax - L_j clocks and then loads normally, so all lanes finish the
+// IV phase together.  nbits[row] in 0..80, or 0xFF for an unused lane that
+// must end in the all-zero state (from_scalar_states, mickey.py:306-316).
+// mat rows: [0, Lmax+80) input words; [Lmax+80, 2 Lmax+80) activity masks
+// (bit j set once lane j has started); row 2 Lmax+80: final lane mask.
+__global__ void __launch_bounds__(BLOCK)
+pack_ragged_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__ ivs, uint32_t iv_stride,
+                   const uint8_t *__restrict__ nbits, int lmax, uint64_t N, uint64_t G,
+                   uint32_t *__restrict__ mat)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    uint32_t used = 0;
+    int len[32];
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+        const uint64_t row = 32 * g + j;
+        const int l = row < N ? nbits[row] : 0xFF;
+        len[j] = l;
+        if (l <= 80) used |= 1u << j;
+    }
+    for (int c = 0; c < lmax; ++c) {
+        uint32_t w = 0, act = 0;
+        for (int j = 0; j < 32; ++j) {
+            const int l = len[j];
+            if (l > 80) continue;
+            const int start = lmax - l;
+            if (c >= start) {
+                act |= 1u << j;
+                const int cc = c - start;
+                const uint32_t byte = ivs[(32 * g + j) * (uint64_t)iv_stride + (cc >> 3)];
+                w |= ((byte >> (7 - (cc & 7))) & 1u) << j;
+            }
+        }
+        mat[(uint64_t)c * G + g] = w;
+        mat[(uint64_t)(lmax + KEY_BITS + c) * G + g] = act;
+    }
+    mat[(uint64_t)(2 * lmax + KEY_BITS) * G + g] = used;
+    pack_bytes_to_clocks(keys, 10, 32 * g, N, KEY_BITS, mat, G, g, lmax);
+}
+
+// Counter-IV synthetic set: one key for every instance,
+// IV_k = the 80-bit big-endian value of the global instance index
+// k = first + 32 g + j (first % 32 == 0), so load clock c carries bit 79 - c of
+// k: the five low bits are fixed lane patterns, the rest are uniform words.
+__global__ void __launch_bounds__(BLOCK)
+pack_counter_kernel(uint64_t key_hi16, uint64_t key_lo64, uint64_t first, uint64_t G, uint32_t *__restrict__ mat)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    const uint64_t base = first + 32 * g;
+    for (int c = 0; c < 80; ++c) {
+        const int p = 79 - c;
+        uint32_t w;
+        if (p >= 64) w = 0u;
+        else if (p >= 5) w = ((base >> p) & 1ull) ? 0xFFFFFFFFu : 0u;
+        else w = p == 0 ? 0xAAAAAAAAu : p == 1 ? 0xCCCCCCCCu : p == 2 ? 0xF0F0F0F0u : p == 3 ? 0xFF00FF00u : 0xFFFF0000u;
+        mat[(uint64_t)c * G + g] = w;
+    }
+    for (int c = 0; c < 80; ++c) {  // key bit c, MSB-first over the 10 key bytes
+        const int p = 79 - c;
+        const uint64_t bit = p >= 64 ? (key_hi16 >> (p - 64)) & 1ull : (key_lo64 >> p) & 1ull;
+        mat[(uint64_t)(80 + c) * G + g] = bit ? 0xFFFFFFFFu : 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Key/IV load + pre-clock (mickey.py:141-151 / :291-303), 32 instances per
+// thread, one input word per load clock.  RAGGED adds the activity masking
+// described at pack_ragged_kernel.
+// ---------------------------------------------------------------------------
+template <bool RAGGED>
+__global__ void __launch_bounds__(BLOCK, 1)
+init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_t G,
+            uint32_t *__restrict__ state, unsigned long long *__restrict__ acc)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    uint32_t r[NBITS], s[NBITS];
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) r[i] = s[i] = 0u;
+
+    const uint32_t *p = mat + g;
+    int c = 0;
+    if constexpr (RAGGED) {
+        const uint32_t *pa = mat + (uint64_t)(lmax + KEY_BITS) * G + g;
+#pragma unroll 1
+        for (; c < lmax; ++c) {
+            clock<true, true>(r, s, *p);
+            const uint32_t act = *pa;
+#pragma unroll
+            for (int i = 0; i < NBITS; ++i) { r[i] &= act; s[i] &= act; }
+            p += G;
+            pa += G;
+        }
+    }
+#pragma unroll 1
+    for (; c < load_clocks; ++c) {
+        clock<true, true>(r, s, *p);
+        p += G;
+    }
+#pragma unroll 1
+    for (int k = 0; k < PRECLOCKS; ++k) clock<true, false>(r, s, 0u);
+
+    if constexpr (RAGGED) {
+        const uint32_t used = mat[(uint64_t)(2 * lmax + KEY_BITS) * G + g];
+#pragma unroll
+        for (int i = 0; i < NBITS; ++i) { r[i] &= used; s[i] &= used; }
+    }
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        state[(uint64_t)i * G + g] = r[i];
+        state[(uint64_t)(NBITS + i) * G + g] = s[i];
+    }
+    acc[g] = 0ull;
+}
+
+// ---------------------------------------------------------------------------
+// Generic stepping: n CLOCK_KG calls with caller-supplied input words and
+// mixing flag, no output (MickeySliced.clock_kg, mickey.py:329-360).  Used by
+// the host mirror's clock_kg(); not a throughput path.
+// ---------------------------------------------------------------------------
+template <bool MIXING>
+__global__ void __launch_bounds__(BLOCK, 1)
+clock_kernel(uint32_t *__restrict__ state, const uint32_t *__restrict__ in_words, uint64_t n, uint64_t G)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    uint32_t r[NBITS], s[NBITS];
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        r[i] = state[(uint64_t)i * G + g];
+        s[i] = state[(uint64_t)(NBITS + i) * G + g];
+    }
+#pragma unroll 1
+    for (uint64_t c = 0; c < n; ++c) clock<MIXING, true>(r, s, in_words ? in_words[c * G + g] : 0u);
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        state[(uint64_t)i * G + g] = r[i];
+        state[(uint64_t)(NBITS + i) * G + g] = s[i];
+    }
+}
+
+// 64-bit accumulate on the FMA pipe (IMAD.WIDE.U32) so the checksum does not
+// take ALU-pipe slots from the LOP3 stream.
+__device__ __forceinline__ void acc_add(unsigned long long &acc, uint32_t z)
+{
+    asm("mad.wide.u32 %0, %1, 1, %0;" : "+l"(acc) : "r"(z));
+}
+
+// ---------------------------------------------------------------------------
+// Keystream, column-major: out[t * stride + g] = z_t (mickey.py:362-368; the
+// compiled loop kernels.py:46-95).  Resumable: state and the checksum
+// accumulator are loaded and stored back.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(BLOCK, 1)
+gen_colmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc,
+                    uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    uint32_t r[NBITS], s[NBITS];
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        r[i] = state[(uint64_t)i * G + g];
+        s[i] = state[(uint64_t)(NBITS + i) * G + g];
+    }
+    unsigned long long a = acc[g];
+    uint32_t *p = out + g;
+#pragma unroll 1
+    for (uint64_t t = 0; t < T; ++t) {
+        const uint32_t z = keystream_word(r, s);
+        *p = z;
+        p += stride;
+        acc_add(a, z);
+        clock<false, false>(r, s, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        state[(uint64_t)i * G + g] = r[i];
+        state[(uint64_t)(NBITS + i) * G + g] = s[i];
+    }
+    acc[g] = a;
+}
+
+// ---------------------------------------------------------------------------
+// Keystream, row-major: out[(32 g + j) * pitch + t / 8], MSB-first bytes
+// (kernels.py:604-621, bitops.py:20-23).
+//
+// Every 8 clocks the thread transposes its 8 keystream words (8 x 32 bits) in
+// registers into 32 output bytes (word k, byte q = instance 8q + k), and parks
+// the 8 words in its private shared-memory column (conflict-free: the word
+// index varies with tid).  After 16 such groups (128 clocks) it reads them
+// back per k, regroups bytes -> words with PRMT (4x4 byte transposes) and
+// issues one 16-byte store per instance row.  Shared memory is only a register
+// extension here (the 200 state words leave no room for 128 more), each thread
+// reads back only what it wrote, so no barrier is needed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
+{
+    return __byte_perm(a, b, sel);
+}
+
+// x[0..3]: words of 4 consecutive groups for fixed k; y[q] = bytes q of x[0..3]
+// in ascending group (= address) order.
+__device__ __forceinline__ void bytes4x4(const uint32_t (&x)[4], uint32_t (&y)[4])
+{
+    const uint32_t a01 = prmt(x[0], x[1], 0x5140);  // [x0.b0, x1.b0, x0.b1, x1.b1]
+    const uint32_t a23 = prmt(x[2], x[3], 0x5140);
+    const uint32_t b01 = prmt(x[0], x[1], 0x7362);  // [x0.b2, x1.b2, x0.b3, x1.b3]
+    const uint32_t b23 = prmt(x[2], x[3], 0x7362);
+    y[0] = prmt(a01, a23, 0x5410);
+    y[1] = prmt(a01, a23, 0x7632);
+    y[2] = prmt(b01, b23, 0x5410);
+    y[3] = prmt(b01, b23, 0x7632);
+}
+
+template <bool ALIGNED16>
+__global__ void __launch_bounds__(BLOCK, 1)
+gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc, uint8_t *__restrict__ out,
+                    uint64_t pitch, uint64_t N, uint64_t G, uint64_t T)
+{
+    extern __shared__ uint32_t tile[];  // [8 k][ROW_GROUPS][BLOCK]
+    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    if (g >= G) return;
+    uint32_t r[NBITS], s[NBITS];
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        r[i] = state[(uint64_t)i * G + g];
+        s[i] = state[(uint64_t)(NBITS + i) * G + g];
+    }
+    unsigned long long a = acc[g];
+    uint32_t *col = tile + threadIdx.x;
+    uint8_t *rows = out + 32 * g * pitch;
+    const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;  // rows of this group that exist
+
+#pragma unroll 1
+    for (uint64_t t0 = 0; t0 < T; t0 += 8 * ROW_GROUPS) {
+        const int ngrp = (T - t0) >= 8 * ROW_GROUPS ? ROW_GROUPS : (int)((T - t0) >> 3);
+#pragma unroll 1
+        for (int grp = 0; grp < ngrp; ++grp) {
+            uint32_t z[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const uint32_t zz = keystream_word(r, s);
+                z[7 - m] = zz;  // clock t0 + 8 grp + m lands in bit 7 - m of the byte (MSB-first)
+                acc_add(a, zz);
+                clock<false, false>(r, s, 0u);
+            }
+            transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
+#pragma unroll
+            for (int k = 0; k < 8; ++k) col[(k * ROW_GROUPS + grp) * BLOCK] = z[k];
+        }
+        // ---- drain: 16 bytes (or the tail) per instance row
+        uint8_t *dst = rows + (t0 >> 3);
+        if (ALIGNED16 && ngrp == ROW_GROUPS && nrows == 32) {
+#pragma unroll 2
+            for (int k = 0; k < 8; ++k) {
+                uint32_t y[4][4];  // [g4][q]
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                    uint32_t x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[u] = col[(k * ROW_GROUPS + 4 * g4 + u) * BLOCK];
+                    bytes4x4(x, y[g4]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * q + k) * pitch) =
+                        make_uint4(y[0][q], y[1][q], y[2][q], y[3][q]);
+            }
+        } else {
+            // ragged edge: short tail, partial last group or unaligned rows
+#pragma unroll 1
+            for (int k = 0; k < 8; ++k)
+#pragma unroll 1
+                for (int grp = 0; grp < ngrp; ++grp) {
+                    const uint32_t x = col[(k * ROW_GROUPS + grp) * BLOCK];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((uint64_t)(8 * q + k) < nrows)
+                            dst[(uint64_t)(8 * q + k) * pitch + grp] = (uint8_t)(x >> (8 * q));
+                }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        state[(uint64_t)i * G + g] = r[i];
+        state[(uint64_t)(NBITS + i) * G + g] = s[i];
+    }
+    acc[g] = a;
+}
+
+// ---------------------------------------------------------------------------
+// Checksum fold: sum_g acc[g] << (32 * ((g + g_offset) & 1))  mod 2^64, i.e. the
+// column-major buffer of everything emitted so far, read as little-endian
+// uint64 words and summed (the cross-GPU invariant of SURVEY.md 8(e)).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(BLOCK)
+checksum_kernel(const unsigned long long *__restrict__ acc, uint64_t G, uint64_t g_offset,
+                unsigned long long *__restrict__ result)
+{
+    unsigned long long v = 0;
+    for (uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; g < G; g += (uint64_t)gridDim.x * BLOCK)
+        v += acc[g] << (32 * ((g + g_offset) & 1));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(result, v);
+}
+
+// ---------------------------------------------------------------------------
+// LOP3 issue-rate probe: the roofline denominator.  16
+// independent non-linear chains per thread, nothing but LOP3 in the loop.
+// lane-ops = threads * iters * 16 * UNROLL.
+// ---------------------------------------------------------------------------
+constexpr int PEAK_UNROLL = 16;
+__global__ void __launch_bounds__(BLOCK)
+lop3_peak_kernel(uint32_t *__restrict__ out, uint32_t seed, int iters)
+{
+    uint32_t x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = seed * (2654435761u + k) + threadIdx.x * (k + 1) + blockIdx.x;
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < PEAK_UNROLL; ++u) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) x[k] = lop3<0x6A>(x[k], x[(k + 5) & 15], x[(k + 11) & 15]);  // c ^ (a & b)
+        }
+    }
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v ^= x[k];
+    if (v == 0x12345u) out[blockIdx.x * BLOCK + threadIdx.x] = v;  // practically never: keeps the chains live
+}
+
+}  // namespace mk2

@@ -1,0 +1,219 @@
+"""Bulk generator: the reference's sliced MICKEY engine lifted to N >> 64.
+
+`MickeyGenerator` owns one C-ABI context (include/mk2.h) = one GPU, one
+stream, the column-major state of N instances.  It is the object the
+reference-shaped front ends (`mickey.MickeySliced`, `kernels.mickey_sliced_words`)
+are thin views of.  All cipher work happens in the CUDA kernels; this module
+only validates arguments, allocates buffers and passes pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from ._native import MK2_IV_UNUSED, check
+
+KEY_BYTES = 10
+IV_MAX_BITS = 80
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(buf) -> int:
+    """Raw address of a numpy array / torch tensor / int pointer."""
+    if buf is None:
+        return 0
+    if isinstance(buf, int):
+        return buf
+    if isinstance(buf, np.ndarray):
+        if not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError("buffer must be C-contiguous")
+        return buf.ctypes.data
+    if _is_torch(buf):
+        if not buf.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return buf.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(buf)!r}")
+
+
+class MickeyGenerator:
+    """N independent MICKEY 2.0 instances on one B200 (32 per GPU thread)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self._lib = _native.lib()
+        self._ctx = C.c_void_p()
+        check(self._lib.mk2_create(int(device), C.byref(self._ctx)), None, "mk2_create")
+        self.device = int(device)
+        if stream is not None:
+            self.set_stream(stream)
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_ctx", None) is not None and self._ctx:
+            self._lib.mk2_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _ck(self, rc, what):
+        check(rc, self._ctx, what)
+
+    def set_stream(self, cuda_stream: Optional[int]):
+        """Launch on an external CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._ck(self._lib.mk2_set_stream(self._ctx, C.c_void_p(cuda_stream or 0)), "mk2_set_stream")
+
+    def set_async(self, flag: bool):
+        self._ck(self._lib.mk2_set_async(self._ctx, int(bool(flag))), "mk2_set_async")
+
+    def synchronize(self):
+        self._ck(self._lib.mk2_sync(self._ctx), "mk2_sync")
+
+    def set_group_offset(self, group_offset: int):
+        self._ck(self._lib.mk2_set_group_offset(self._ctx, int(group_offset)), "mk2_set_group_offset")
+
+    # -- geometry ---------------------------------------------------------
+    def _query(self):
+        n, g, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._ck(self._lib.mk2_query(self._ctx, C.byref(n), C.byref(g), C.byref(c)), "mk2_query")
+        return n.value, g.value, c.value
+
+    @property
+    def instances(self) -> int:
+        return self._query()[0]
+
+    @property
+    def groups(self) -> int:
+        return self._query()[1]
+
+    @property
+    def clocks(self) -> int:
+        return self._query()[2]
+
+    # -- initialisation ---------------------------------------------------
+    def init_material(self, keys, ivs=None, iv_bits: int = 0):
+        """Uniform IV length: keys u8[N,10], ivs u8[N,>=ceil(iv_bits/8)] (numpy or torch, host or device)."""
+        n, iv_stride = _material_shape(keys, ivs, iv_bits)
+        self._ck(self._lib.mk2_init_from_material(self._ctx, _ptr(keys), _ptr(ivs) if iv_bits else 0, iv_stride,
+                                                  int(iv_bits), n), "mk2_init_from_material")
+        return self
+
+    def init_ragged(self, keys, ivs, iv_nbits):
+        """Per-instance IV bit lengths (u8[N], 0..80 or MK2_IV_UNUSED)."""
+        n, iv_stride = _material_shape(keys, ivs, 0)
+        if int(np.prod(tuple(iv_nbits.shape))) != n:
+            raise ValueError("iv_nbits must have one entry per instance")
+        self._ck(self._lib.mk2_init_ragged(self._ctx, _ptr(keys), _ptr(ivs), iv_stride, _ptr(iv_nbits), n),
+                 "mk2_init_ragged")
+        return self
+
+    def init_counter(self, key: bytes, first_index: int, n: int):
+        """One key, IV_k = 80-bit big-endian (first_index + k): SURVEY.md 8(d) synthetic set."""
+        if len(key) != KEY_BYTES:
+            raise ValueError(f"key must be {KEY_BYTES} bytes")
+        kb = (C.c_uint8 * KEY_BYTES).from_buffer_copy(bytes(key))
+        self._ck(self._lib.mk2_init_counter_iv(self._ctx, C.cast(kb, C.c_void_p), int(first_index), int(n)),
+                 "mk2_init_counter_iv")
+        return self
+
+    # -- generation -------------------------------------------------------
+    def generate_colmajor(self, nclocks: int, out=None, stride_words: Optional[int] = None):
+        """uint32 out[nclocks][G]; bit j of out[t][g] = keystream bit t of instance 32 g + j."""
+        G = self.groups
+        stride = G if stride_words is None else int(stride_words)
+        if out is None:
+            out = np.empty((nclocks, stride), np.uint32)
+        self._ck(self._lib.mk2_generate_colmajor(self._ctx, int(nclocks), _ptr(out), stride), "mk2_generate_colmajor")
+        return out
+
+    def generate_rowmajor(self, nclocks: int, out=None, pitch_bytes: Optional[int] = None, byte_offset: int = 0):
+        """uint8 out[N][nclocks/8], MSB-first (the reference's lane-major order)."""
+        if nclocks % 8:
+            raise ValueError("bit count must be a multiple of 8")
+        N = self.instances
+        if out is None:
+            pitch = nclocks // 8 if pitch_bytes is None else int(pitch_bytes)
+            out = np.empty((N, pitch), np.uint8)
+        elif pitch_bytes is None:
+            pitch = int(out.shape[-1]) * (out.element_size() if _is_torch(out) else out.itemsize)
+        else:
+            pitch = int(pitch_bytes)
+        self._ck(self._lib.mk2_generate_rowmajor(self._ctx, int(nclocks), _ptr(out) + int(byte_offset), pitch),
+                 "mk2_generate_rowmajor")
+        return out
+
+    def clock(self, mixing: bool, input_words=None, n: int = 1):
+        """n raw CLOCK_KG steps (no output); input_words uint32[n][G] or None."""
+        self._ck(self._lib.mk2_clock(self._ctx, int(bool(mixing)), _ptr(input_words), int(n)), "mk2_clock")
+
+    # -- state / checksum -------------------------------------------------
+    def export_state(self) -> np.ndarray:
+        """uint32 rs[200][G]: R words then S words (MickeySliced.rregs / .sregs)."""
+        rs = np.empty((200, self.groups), np.uint32)
+        self._ck(self._lib.mk2_state_export(self._ctx, _ptr(rs)), "mk2_state_export")
+        return rs
+
+    def import_state(self, rs, n: int):
+        rs = np.ascontiguousarray(rs, np.uint32) if isinstance(rs, np.ndarray) else rs
+        self._ck(self._lib.mk2_state_import(self._ctx, _ptr(rs), int(n)), "mk2_state_import")
+        return self
+
+    def checksum(self) -> int:
+        v = C.c_uint64()
+        self._ck(self._lib.mk2_checksum(self._ctx, C.byref(v)), "mk2_checksum")
+        return v.value
+
+    # -- measurement ------------------------------------------------------
+    @property
+    def last_kernel_ms(self) -> float:
+        return float(self._lib.mk2_last_kernel_ms(self._ctx))
+
+    @property
+    def last_kernel_launches(self) -> int:
+        return int(self._lib.mk2_last_kernel_launches(self._ctx))
+
+    def lop3_peak(self):
+        """(lane-ops/s, ms) of the dependency-free LOP3 probe: the roofline denominator."""
+        v, ms = C.c_double(), C.c_float()
+        self._ck(self._lib.mk2_lop3_peak(self._ctx, C.byref(v), C.byref(ms)), "mk2_lop3_peak")
+        return v.value, ms.value
+
+
+def _material_shape(keys, ivs, iv_bits):
+    kshape = tuple(keys.shape)
+    if len(kshape) != 2 or kshape[1] != KEY_BYTES:
+        raise ValueError(f"keys must have shape [N, {KEY_BYTES}]")
+    if _dtype_name(keys) != "uint8":
+        raise ValueError("keys must be uint8")
+    n = kshape[0]
+    if n < 1:
+        raise ValueError("at least one lane is required")
+    if iv_bits > IV_MAX_BITS:
+        raise ValueError(f"IV must be at most {IV_MAX_BITS} bits")
+    iv_stride = 0
+    if ivs is not None:
+        ishape = tuple(ivs.shape)
+        if len(ishape) != 2 or ishape[0] != n or _dtype_name(ivs) != "uint8":
+            raise ValueError("ivs must be uint8 with shape [N, iv_bytes]")
+        iv_stride = ishape[1]
+    if iv_bits and iv_stride < (iv_bits + 7) // 8:
+        raise ValueError("ivs rows are shorter than iv_bits")
+    return n, iv_stride
+
+
+def _dtype_name(x) -> str:
+    return str(x.dtype).replace("torch.", "")

@@ -1,0 +1,142 @@
+"""Pins the CPU oracle (oracle/mickey_oracle.c) to the reference.
+
+Every expected value comes from tests/golden/mickey_golden.json, which
+oracle/gen_golden.py produced by running the reference package itself, or
+from the eSTREAM vectors the reference embeds (vectors.py:41-60).  CPU only.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_material
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def bits_int(bits):
+    return sum(int(b) << i for i, b in enumerate(bits))
+
+
+def test_tables_match_reference(oracle, golden):
+    t = oracle.tables()
+    g = golden["tables"]
+    assert [i for i, b in enumerate(t["RTAPS"]) if b] == g["RTAPS"]
+    assert len(g["RTAPS"]) == 50  # tests/test_mickey.py:28-35
+    for name in ("COMP0", "COMP1", "FB0", "FB1"):
+        assert t[name] == g[name]
+    assert t["COMP0"][0] == t["COMP0"][99] == t["COMP1"][0] == t["COMP1"][99] == 0
+
+
+def test_estream_vectors_scalar(oracle, golden):
+    for rec in golden["kats"]:
+        st = oracle.Scalar.from_key_iv(bytes.fromhex(rec["key"]), bytes.fromhex(rec["iv"]))
+        assert f"{bits_int(st.r):x}" == rec["post_init_r"]
+        assert f"{bits_int(st.s):x}" == rec["post_init_s"]
+        assert st.keystream_bytes(16).hex() == rec["ks"]
+
+
+@pytest.mark.parametrize("width", [32, 64])
+def test_estream_vectors_every_lane(oracle, golden, width):
+    # vectors.verify_vectors: every lane of the sliced engine (vectors.py:189-197)
+    for rec in golden["kats"]:
+        mats = [(bytes.fromhex(rec["key"]), bytes.fromhex(rec["iv"]))] * width
+        words = oracle.sliced_words(mats, 128, width)
+        full = (1 << width) - 1
+        assert set(int(w) for w in words) <= {0, full}
+        lane_bits = ((words >> np.uint64(width - 1)) & np.uint64(1)).astype(np.uint8)
+        assert np.packbits(lane_bits).tobytes() == bytes.fromhex(rec["ks"])
+
+
+def test_scalar_cases(oracle, golden):
+    for rec in golden["scalar_cases"]:
+        key, iv = golden_material(rec)
+        st = oracle.Scalar.from_key_iv(key, iv)
+        assert f"{bits_int(st.r):x}" == rec["post_init_r"]
+        assert f"{bits_int(st.s):x}" == rec["post_init_s"]
+        assert st.keystream_bytes(256).hex() == rec["ks256"]
+
+
+def test_zero_state_clock_and_trace(oracle, golden):
+    st = oracle.Scalar()
+    st.clock_kg(False, 0)
+    assert f"{bits_int(st.r):x}" == golden["zero_state_one_clock"]["r"]
+    assert f"{bits_int(st.s):x}" == golden["zero_state_one_clock"]["s"]
+    k = golden["kats"][0]
+    st = oracle.Scalar.from_key_iv(bytes.fromhex(k["key"]), bytes.fromhex(k["iv"]))
+    for r_hex, s_hex in golden["kat0_state_trace_100"]:
+        st.clock_kg(False, 0)
+        assert f"{bits_int(st.r):x}" == r_hex and f"{bits_int(st.s):x}" == s_hex
+
+
+def test_sliced_cases(oracle, golden):
+    for case in golden["sliced_cases"]:
+        mats = [golden_material(m) for m in case["materials"]]
+        eng = oracle.Sliced.from_key_ivs(mats)
+        width = case["width"]
+        mask = (1 << width) - 1
+        # lanes >= width of the 64-lane oracle hold padding; compare the low `width` lanes
+        assert [f"{w & mask:x}" for w in eng.rregs] == [f"{int(x, 16) & mask:x}" for x in case["init_state"]["r"]], case["name"]
+        assert [f"{w & mask:x}" for w in eng.sregs] == [f"{int(x, 16) & mask:x}" for x in case["init_state"]["s"]], case["name"]
+        words = oracle.sliced_words(mats, case["nclocks"], width)
+        assert sha(words.astype("<u8").tobytes()) == case["words_sha256"], case["name"]
+        if case["words_hex"]:
+            assert words.astype("<u8").tobytes().hex() == case["words_hex"]
+        # resumable engine agrees with the restart-only loop (mickey.py:362 vs kernels.py:46)
+        stepped = eng.keystream_words(case["nclocks"]) & np.uint64(mask)
+        assert np.array_equal(stepped, words)
+
+
+def test_c1_lockstep_million(oracle, golden):
+    rec = golden["kats"][0]
+    mats = [(bytes.fromhex(rec["key"]), bytes.fromhex(rec["iv"]))] * 32
+    words = oracle.sliced_words(mats, 1_000_000, 32)
+    assert sha(words.astype("<u4").tobytes()) == rec["c1_words_u4_sha256"]
+    lane0 = np.packbits((words & np.uint64(1)).astype(np.uint8)).tobytes()
+    assert sha(lane0) == rec["c1_lane0_sha256"]
+    assert lane0[-16:].hex() == rec["c1_lane0_tail16"]
+
+
+def test_bench_seed_lanes(oracle, golden):
+    b = golden["bench_seed"]
+    mats = [golden_material(m) for m in b["materials"]]
+    keys, ivs, nb = oracle.pack_materials(mats)
+    col = oracle.bulk_colmajor(keys, ivs, 80, b["nclocks"])
+    assert sha(col.tobytes()) == b["words_u8_sha256"]
+    assert f"{oracle.checksum_colmajor(col):x}" == b["u64_wrap_sum"]
+    row = oracle.bulk_rowmajor(keys, ivs, 80, b["nclocks"] // 8 * 8)
+    assert sha(row.tobytes()) == b["lane_major_sha256"]
+    assert row[0, :16].tobytes().hex() == b["lane0_first16"]
+
+
+def test_counter_iv_sets(oracle, golden):
+    for c in golden["counter_iv"]:
+        keys, ivs = oracle.counter_material(bytes.fromhex(c["key"]), c["first"], c["n"])
+        col = oracle.bulk_colmajor(keys, ivs, 80, c["nclocks"])
+        row = oracle.bulk_rowmajor(keys, ivs, 80, c["nclocks"])
+        assert sha(col.tobytes()) == c["colmajor_sha256"]
+        assert sha(row.tobytes()) == c["rowmajor_sha256"]
+        assert row[0, :16].tobytes().hex() == c["lane0_first16"]
+        assert row[-1, :16].tobytes().hex() == c["lane_last_first16"]
+        assert f"{oracle.checksum_colmajor(col):x}" == c["u64_wrap_sum"]
+        assert f"{int(np.bitwise_xor.reduce(np.ascontiguousarray(col).view('<u8').ravel())):x}" == c["xor_fold"]
+
+
+def test_bulk_ragged_and_partial_batches(oracle):
+    # bulk layouts agree with per-lane scalar streams, incl. N not a multiple of 32/64
+    rng = np.random.default_rng(7)
+    N, T = 150, 264
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    nbits = rng.integers(0, 81, N, dtype=np.uint8)
+    row = oracle.bulk_rowmajor(keys, ivs, nbits, T)
+    col = oracle.bulk_colmajor(keys, ivs, nbits, T)
+    assert col.shape == (T, 5)
+    for n in (0, 31, 32, 63, 64, 100, 149):
+        bits = np.unpackbits(ivs[n])[: nbits[n]].tolist()
+        ks = oracle.Scalar.from_key_iv(keys[n].tobytes(), bits).keystream_bytes(T // 8)
+        assert row[n].tobytes() == ks
+        lane = ((col[:, n // 32] >> np.uint32(n % 32)) & 1).astype(np.uint8)
+        assert np.packbits(lane).tobytes() == ks
