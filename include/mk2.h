@@ -149,6 +149,10 @@ int mk2_last_kernel_launches(const mk2_ctx *ctx);
  * themselves); mk2_last_kernel_ms is then only valid after mk2_sync. */
 int mk2_set_async(mk2_ctx *ctx, int async);
 
+/* Tuning knob: threads per CTA of the clocking kernels (32..256, step 32;
+ * default 256 = 8 warps per SM at 255 registers per thread). */
+int mk2_set_block_threads(mk2_ctx *ctx, int threads);
+
 /*
  * Roofline probe: sustained LOP3 lane-operations per second of this device,
  * measured with a dependency-free LOP3 kernel.

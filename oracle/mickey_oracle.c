@@ -170,11 +170,11 @@ void mk2o_sliced_clock(mk2o_sliced *st, int mixing, uint64_t in)
  * all-zero material (they behave as zero key / empty-or-zero IV lanes of the
  * same clock count, exactly as the reference's unused lanes do).
  * Returns 0, or -(lane+1) when a lane's IV is longer than 80 bits. */
-int mk2o_sliced_init(mk2o_sliced *st, const uint8_t *keys, const uint8_t *ivs, int iv_stride,
-                     const uint8_t *iv_nbits, int n)
+int mk2o_sliced_init2(mk2o_sliced *st, const uint8_t *keys, const uint8_t *ivs, int iv_stride,
+                      const uint8_t *iv_nbits, int n, int force_ragged)
 {
     if (n < 1 || n > 64) return -1000;
-    int uniform = 1;
+    int uniform = !force_ragged;
     for (int j = 0; j < n; ++j) {
         if (iv_nbits[j] > 80) return -(j + 1);
         if (iv_nbits[j] != iv_nbits[0]) uniform = 0;
@@ -203,6 +203,12 @@ int mk2o_sliced_init(mk2o_sliced *st, const uint8_t *keys, const uint8_t *ivs, i
     }
     for (int c = 0; c < 100; ++c) mk2o_sliced_clock(st, 1, 0);
     return 0;
+}
+
+int mk2o_sliced_init(mk2o_sliced *st, const uint8_t *keys, const uint8_t *ivs, int iv_stride,
+                     const uint8_t *iv_nbits, int n)
+{
+    return mk2o_sliced_init2(st, keys, ivs, iv_stride, iv_nbits, n, 0);
 }
 
 /* mickey.py:362-368 keystream_words (resumable, state advances) */
@@ -286,9 +292,12 @@ static void batch_words(const uint8_t *keys, const uint8_t *ivs, int iv_stride, 
     uint8_t lens[64];
     for (int j = 0; j < n; ++j) lens[j] = iv_uniform >= 0 ? (uint8_t)iv_uniform : iv_nbits[first + j];
     mk2o_sliced st;
-    /* uniform route pads the unused lanes with zero bits of the same length,
-     * like the reference; ragged route leaves them in the zero state. */
-    mk2o_sliced_init(&st, keys + 10 * first, ivs + (size_t)iv_stride * first, iv_stride, lens, n);
+    /* uniform call (one IV length for the whole set): word-wide route, unused
+     * lanes load zero bits for the same clock count; per-lane lengths: always
+     * the scalar route, unused lanes stay in the zero state -- the two routes of
+     * mickey.py:287-303, chosen per CALL so padding does not depend on how a
+     * ragged set happens to fall into 64-lane batches. */
+    mk2o_sliced_init2(&st, keys + 10 * first, ivs + (size_t)iv_stride * first, iv_stride, lens, n, iv_uniform < 0);
     /* no lane mask at width 64 (kernels.py:196-200): unused lanes keep the
      * keystream of their padding material, exactly as in the reference */
     mk2o_sliced_loop(st.r, st.s, words, T + (T & 1));
@@ -392,17 +401,20 @@ typedef struct {
     const uint64_t *r, *s;
     uint64_t *o;
     uint64_t nclocks;
+    int ncalls;
 } loop_job;
 
 static void *loop_worker(void *arg)
 {
     loop_job *lj = (loop_job *)arg;
-    mk2o_sliced_loop(lj->r, lj->s, lj->o, lj->nclocks);
+    for (int c = 0; c < lj->ncalls; ++c) mk2o_sliced_loop(lj->r, lj->s, lj->o, lj->nclocks);
     return NULL;
 }
 
+/* ncalls back-to-back runs of the loop per worker over the same scratch (the
+ * reference's `repeats`), so the sample size is not bounded by memory. */
 uint64_t mk2o_timed_loops(const uint64_t *r, const uint64_t *s, uint64_t *scratch, uint64_t nclocks,
-                          int nworkers)
+                          int ncalls, int nworkers)
 {
     build_masks();
     if (nworkers < 1) nworkers = 1;
@@ -415,7 +427,7 @@ uint64_t mk2o_timed_loops(const uint64_t *r, const uint64_t *s, uint64_t *scratc
         return 0;
     }
     for (int w = 0; w < nworkers; ++w) {
-        jobs[w] = (loop_job){r + (size_t)w * NB, s + (size_t)w * NB, scratch + (size_t)w * nclocks, nclocks};
+        jobs[w] = (loop_job){r + (size_t)w * NB, s + (size_t)w * NB, scratch + (size_t)w * nclocks, nclocks, ncalls};
         if (w > 0 && pthread_create(&th[w], NULL, loop_worker, &jobs[w]) != 0) loop_worker(&jobs[w]), th[w] = 0;
     }
     loop_worker(&jobs[0]);

@@ -55,7 +55,7 @@ def lib() -> C.CDLL:
             f = getattr(L, name)
             f.argtypes = [u8p, u8p, C.c_int, u8p, C.c_int, C.c_uint64, C.c_uint64, outp, C.c_int]
             f.restype = C.c_int
-        L.mk2o_timed_loops.argtypes = [u64p, u64p, u64p, C.c_uint64, C.c_int]
+        L.mk2o_timed_loops.argtypes = [u64p, u64p, u64p, C.c_uint64, C.c_int, C.c_int]
         L.mk2o_timed_loops.restype = C.c_uint64
         L.mk2o_checksum_colmajor.argtypes = [u32p, C.c_uint64, C.c_uint64, C.c_uint64]
         L.mk2o_checksum_colmajor.restype = C.c_uint64
@@ -237,10 +237,10 @@ def counter_material(key: bytes, first: int, n: int):
     return keys, ivs
 
 
-def timed_loops(nclocks: int, nworkers: int, states: np.ndarray | None = None):
-    """Run `nworkers` independent 64-lane keystream loops of `nclocks` clocks
-    (the region the reference's bench times, bench.py:169-183).  Returns
-    seconds elapsed."""
+def timed_loops(nclocks: int, nworkers: int, ncalls: int = 1, states: np.ndarray | None = None):
+    """Run `nworkers` independent 64-lane keystream loops, each `ncalls` calls of
+    `nclocks` clocks (the region the reference's bench times,
+    bench.py:169-183, repeated like its `repeats`).  Returns seconds elapsed."""
     import time
 
     if states is None:
@@ -252,7 +252,7 @@ def timed_loops(nclocks: int, nworkers: int, states: np.ndarray | None = None):
     scratch = np.zeros((nworkers, nclocks), np.uint64)
     scratch[:] = 1  # touch pages outside the timed region
     t0 = time.perf_counter()
-    lib().mk2o_timed_loops(_p(r, u64p), _p(s, u64p), _p(scratch, u64p), nclocks, nworkers)
+    lib().mk2o_timed_loops(_p(r, u64p), _p(s, u64p), _p(scratch, u64p), nclocks, ncalls, nworkers)
     return time.perf_counter() - t0
 
 

@@ -45,6 +45,7 @@ SYMBOLS = {
     "mk2_last_kernel_ms": (C.c_float, [_vp]),
     "mk2_last_kernel_launches": (C.c_int, [_vp]),
     "mk2_set_async": (C.c_int, [_vp, C.c_int]),
+    "mk2_set_block_threads": (C.c_int, [_vp, C.c_int]),
     "mk2_lop3_peak": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
     "mk2_lop3_per_clock": (C.c_int, []),
 }

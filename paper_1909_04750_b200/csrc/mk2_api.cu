@@ -34,6 +34,7 @@ struct mk2_ctx {
     bool ready = false, async = false, timing_open = false;
     float last_ms = 0.f;
     int last_launches = 0;
+    int block = BLOCK;  // threads per CTA of the clocking kernels (tunable, <= BLOCK)
     std::string err;
 };
 
@@ -64,7 +65,7 @@ bool is_device_ptr(const void *p)
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-inline unsigned blocks_for(uint64_t G) { return (unsigned)((G + BLOCK - 1) / BLOCK); }
+inline unsigned blocks_for(uint64_t G, int block = BLOCK) { return (unsigned)((G + block - 1) / block); }
 
 int begin_timing(mk2_ctx *ctx)
 {
@@ -136,11 +137,11 @@ int stage_input(mk2_ctx *ctx, const void *src, size_t bytes, const uint8_t **dev
 
 int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bool ragged)
 {
-    const unsigned nb = blocks_for(ctx->G);
+    const unsigned nb = blocks_for(ctx->G, ctx->block);
     if (ragged)
-        init_kernel<true><<<nb, BLOCK, 0, ctx->stream>>>(mat, load_clocks, lmax, ctx->G, ctx->d_state, ctx->d_acc);
+        init_kernel<true><<<nb, ctx->block, 0, ctx->stream>>>(mat, load_clocks, lmax, ctx->G, ctx->d_state, ctx->d_acc);
     else
-        init_kernel<false><<<nb, BLOCK, 0, ctx->stream>>>(mat, load_clocks, lmax, ctx->G, ctx->d_state, ctx->d_acc);
+        init_kernel<false><<<nb, ctx->block, 0, ctx->stream>>>(mat, load_clocks, lmax, ctx->G, ctx->d_state, ctx->d_acc);
     CK(cudaGetLastError());
     ctx->last_launches++;
     ctx->clocks = 0;
@@ -150,7 +151,7 @@ int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bo
 
 int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 {
-    gen_colmajor_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, stride,
+    gen_colmajor_kernel<<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, stride,
                                                                        ctx->G, T);
     CK(cudaGetLastError());
     ctx->last_launches++;
@@ -161,10 +162,10 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch)
 {
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
     if (aligned)
-        gen_rowmajor_kernel<true><<<blocks_for(ctx->G), BLOCK, ROW_SMEM_BYTES, ctx->stream>>>(
+        gen_rowmajor_kernel<true><<<blocks_for(ctx->G, ctx->block), ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
             ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T);
     else
-        gen_rowmajor_kernel<false><<<blocks_for(ctx->G), BLOCK, ROW_SMEM_BYTES, ctx->stream>>>(
+        gen_rowmajor_kernel<false><<<blocks_for(ctx->G, ctx->block), ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
             ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T);
     CK(cudaGetLastError());
     ctx->last_launches++;
@@ -284,6 +285,14 @@ int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream)
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own;
+    return MK2_OK;
+}
+
+int mk2_set_block_threads(mk2_ctx *ctx, int threads)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (threads < 32 || threads > BLOCK || threads % 32) return fail(ctx, MK2_E_ARG, "threads per CTA must be 32..256 in steps of 32");
+    ctx->block = threads;
     return MK2_OK;
 }
 
@@ -521,9 +530,9 @@ int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n)
     if ((rc = stage_input(ctx, input_words, input_words ? sizeof(uint32_t) * n * ctx->G : 0, &din, &owned))) return rc;
     const uint32_t *w = reinterpret_cast<const uint32_t *>(din);
     if (mixing)
-        clock_kernel<true><<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
+        clock_kernel<true><<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
     else
-        clock_kernel<false><<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
+        clock_kernel<false><<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
     CK(cudaGetLastError());
     ctx->last_launches++;
     if (owned) CK(cudaFreeAsync(owned, ctx->stream));

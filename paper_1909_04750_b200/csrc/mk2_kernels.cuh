@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(BLOCK)
 pack_uniform_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__ ivs, uint32_t iv_stride,
                     int iv_bits, uint64_t N, uint64_t G, uint32_t *__restrict__ mat)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     pack_bytes_to_clocks(ivs, iv_stride, 32 * g, N, iv_bits, mat, G, g, 0);
     pack_bytes_to_clocks(keys, 10, 32 * g, N, KEY_BITS, mat, G, g, iv_bits);
@@ -108,7 +108,7 @@ pack_ragged_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__
                    const uint8_t *__restrict__ nbits, int lmax, uint64_t N, uint64_t G,
                    uint32_t *__restrict__ mat)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     uint32_t used = 0;
     int len[32];
@@ -146,7 +146,7 @@ pack_ragged_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__
 __global__ void __launch_bounds__(BLOCK)
 pack_counter_kernel(uint64_t key_hi16, uint64_t key_lo64, uint64_t first, uint64_t G, uint32_t *__restrict__ mat)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     const uint64_t base = first + 32 * g;
     for (int c = 0; c < 80; ++c) {
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
 init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_t G,
             uint32_t *__restrict__ state, unsigned long long *__restrict__ acc)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     uint32_t r[NBITS], s[NBITS];
 #pragma unroll
@@ -224,7 +224,7 @@ template <bool MIXING>
 __global__ void __launch_bounds__(BLOCK, 1)
 clock_kernel(uint32_t *__restrict__ state, const uint32_t *__restrict__ in_words, uint64_t n, uint64_t G)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     uint32_t r[NBITS], s[NBITS];
 #pragma unroll
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
 gen_colmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc,
                     uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     uint32_t r[NBITS], s[NBITS];
 #pragma unroll
@@ -321,7 +321,7 @@ gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict
                     uint64_t pitch, uint64_t N, uint64_t G, uint64_t T)
 {
     extern __shared__ uint32_t tile[];  // [8 k][ROW_GROUPS][BLOCK]
-    const uint64_t g = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
     uint32_t r[NBITS], s[NBITS];
 #pragma unroll

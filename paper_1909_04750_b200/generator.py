@@ -80,6 +80,10 @@ class MickeyGenerator:
     def set_async(self, flag: bool):
         self._ck(self._lib.mk2_set_async(self._ctx, int(bool(flag))), "mk2_set_async")
 
+    def set_block_threads(self, threads: int):
+        """Tuning knob: threads per CTA of the clocking kernels (32..256)."""
+        self._ck(self._lib.mk2_set_block_threads(self._ctx, int(threads)), "mk2_set_block_threads")
+
     def synchronize(self):
         self._ck(self._lib.mk2_sync(self._ctx), "mk2_sync")
 

@@ -1,0 +1,139 @@
+"""CPU-only checks of the host mirror and the C-ABI library (no compute calls)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1909_04750_b200 as pkg
+from paper_1909_04750_b200 import _native, kernels, mickey, sharding
+from paper_1909_04750_b200.mickey import MickeyKeyIv, MickeyKeyIvError
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    header = (ROOT / "include" / "mk2.h").read_text()
+    declared = set(re.findall(r"\b(mk2_[a-z0-9_]+)\s*\(", header))
+    declared.discard("mk2_ctx")
+    assert declared, "no declarations parsed from include/mk2.h"
+    L = C.CDLL(str(_native.library_path()))
+    for name in sorted(declared):
+        assert hasattr(L, name), f"libmk2.so does not export {name}"
+    assert declared == set(_native.SYMBOLS), "ctypes table out of sync with include/mk2.h"
+    assert _native.lib().mk2_abi_version() == 1
+    assert _native.lib().mk2_lop3_per_clock() == 327
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(pkg.Mk2Error, match="no CPU fallback"):
+        pkg.MickeyGenerator(0)
+    with pytest.raises(pkg.Mk2Error):
+        pkg.mickey_sliced_words([MickeyKeyIv(bytes(10), b"")], 8)
+
+
+def test_product_package_never_imports_oracle():
+    for path in (ROOT / "paper_1909_04750_b200").rglob("*.py"):
+        text = path.read_text()
+        assert "import oracle" not in text and "from oracle" not in text, path
+    for path in (ROOT / "paper_1909_04750_b200" / "csrc").glob("*.cu*"):
+        assert "oracle" not in path.read_text(), path
+
+
+def test_constants_structure(golden):
+    c = mickey.mickey_constants()
+    assert len(c["RTAPS"]) == 50
+    assert list(c["RTAPS"]) == golden["tables"]["RTAPS"]
+    for name in ("COMP0", "COMP1", "FB0", "FB1"):
+        assert list(c[name]) == golden["tables"][name]
+    assert mickey.COMP0[0] == mickey.COMP0[99] == mickey.COMP1[0] == mickey.COMP1[99] == 0
+
+
+def test_cuda_tables_match_python_tables():
+    src = (ROOT / "paper_1909_04750_b200" / "csrc" / "mk2_clock.cuh").read_text()
+    words = [int(x, 16) for x in re.findall(r"case \d+: return (0x[0-9A-Fa-f]+)u;", src)]
+    assert len(words) == 20
+    expect = mickey._R_MASK_WORDS + mickey._COMP0_WORDS + mickey._COMP1_WORDS + mickey._FB0_WORDS + mickey._FB1_WORDS
+    assert tuple(words) == expect
+
+
+def test_keyiv_validation():
+    # tests/test_mickey.py:93-99
+    with pytest.raises(MickeyKeyIvError):
+        MickeyKeyIv(bytes(10), bytes(11))
+    with pytest.raises(MickeyKeyIvError):
+        MickeyKeyIv(bytes(10), [0] * 81)
+    with pytest.raises(MickeyKeyIvError):
+        MickeyKeyIv(bytes(9), b"")
+    with pytest.raises(MickeyKeyIvError):
+        MickeyKeyIv(bytes(10), [0, 2, 1])
+    m = MickeyKeyIv(bytes(range(10)), b"\xa5")
+    assert m.iv_bits() == [1, 0, 1, 0, 0, 1, 0, 1]
+    assert m.key_bits()[:16] == [0] * 8 + [0, 0, 0, 0, 0, 0, 0, 1]
+    assert isinstance(MickeyKeyIvError("x"), ValueError)
+
+
+def test_pack_materials_errors_name_the_lane():
+    # tests/test_mickey.py:140-145
+    bad = type("Bad", (), {"iv_bits": lambda self: [0] * 81, "key_bits": lambda self: [0] * 80})()
+    mats = [MickeyKeyIv(bytes(10), b"")] * 3 + [bad]
+    with pytest.raises(MickeyKeyIvError, match="lane 3"):
+        mickey.pack_materials(mats, 32)
+    with pytest.raises(MickeyKeyIvError, match="at least one lane"):
+        mickey.pack_materials([], 32)
+    with pytest.raises(MickeyKeyIvError, match="exceed width"):
+        mickey.pack_materials([MickeyKeyIv(bytes(10))] * 33, 32)
+    with pytest.raises(ValueError, match="lane width"):
+        mickey.MickeySliced.from_key_ivs([MickeyKeyIv(bytes(10))], width=48)
+
+
+def test_pack_materials_layout():
+    mats = [MickeyKeyIv(bytes(range(10)), b"\x80\x01"), MickeyKeyIv(bytes(10), [1, 0, 1])]
+    keys, ivs, nbits, uniform = mickey.pack_materials(mats, 32)
+    assert not uniform
+    assert keys[0].tobytes() == bytes(range(10))
+    assert ivs[0, :2].tobytes() == b"\x80\x01" and ivs[1, 0] == 0b10100000
+    assert nbits[:2].tolist() == [16, 3] and set(nbits[2:].tolist()) == {_native.MK2_IV_UNUSED}
+    keys, ivs, nbits, uniform = mickey.pack_materials([mats[0]] * 5, 64)
+    assert uniform and set(nbits.tolist()) == {16} and not keys[5:].any()
+
+
+def test_lane_helpers(golden):
+    # tests/test_kernels.py:75-82
+    h = golden["lane_helpers"]
+    w = np.array(h["words"], dtype=np.uint64)
+    assert kernels.words_to_lane_bits(w, 0).tolist() == h["lane0_bits"]
+    assert kernels.words_to_lane_bits(w, 1).tolist() == h["lane1_bits"]
+    assert kernels.words_to_lane_bytes(w, 0).hex() == h["lane0_msb"]
+    assert kernels.words_to_lane_bytes(w, 0, "lsb").hex() == h["lane0_lsb"]
+    assert kernels.words_lane_major_bytes(w, 2).hex() == h["lane_major_2"]
+    with pytest.raises(ValueError):
+        kernels.words_to_lane_bytes(w, 0, "middle")
+
+
+def test_shard_partition_properties():
+    for n in (0, 1, 31, 32, 33, 1000, 1 << 20, (1 << 20) + 17):
+        for world in (1, 2, 3, 4, 8):
+            shards = [sharding.shard_instances(n, world, r) for r in range(world)]
+            assert sum(s.count for s in shards) == n
+            pos = 0
+            for s in shards:
+                assert s.first == pos or s.count == 0
+                assert s.first % 32 == 0 or s.count == 0
+                assert s.group_offset * 32 == s.first or s.count == 0
+                pos += s.count
+            sizes = [s.groups for s in shards]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        sharding.shard_instances(10, 2, 2)
+
+
+def test_checksum_i64_roundtrip():
+    for u in (0, 1, (1 << 63) - 1, 1 << 63, (1 << 64) - 1, 0xDB93F1AC2EF9D52E):
+        assert sharding.from_i64(sharding.to_i64(u)) == u
+    assert sharding.allreduce_checksum(0xDB93F1AC2EF9D52E) == 0xDB93F1AC2EF9D52E
