@@ -52,9 +52,11 @@ int mk2_device_count(void);
 /* Context = one device, one stream, the state of N instances. */
 int mk2_create(int device, mk2_ctx **out);
 int mk2_destroy(mk2_ctx *ctx);
-/* Launch on the caller's stream (e.g. torch's current stream) instead of the
- * context's own; pass NULL to go back to the private stream. */
+/* Launch on the caller's stream (e.g. torch's current stream; NULL/0 is the
+ * legacy default stream) instead of the context's own non-blocking stream;
+ * mk2_use_own_stream() goes back. */
 int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream);
+int mk2_use_own_stream(mk2_ctx *ctx);
 int mk2_sync(mk2_ctx *ctx);
 const char *mk2_last_error(const mk2_ctx *ctx); /* ctx may be NULL: last create error */
 
@@ -148,6 +150,11 @@ int mk2_last_kernel_launches(const mk2_ctx *ctx);
 /* Skip the per-call event synchronisation (for callers that time the stream
  * themselves); mk2_last_kernel_ms is then only valid after mk2_sync. */
 int mk2_set_async(mk2_ctx *ctx, int async);
+
+/* Tuning knob: clocks per scheduling chunk of the persistent keystream kernels
+ * (>= 128, default 4096): a chain of 1024 instances runs one chunk, parks its
+ * state and goes back to the ready queue. */
+int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
 
 /* Tuning knob: threads per CTA of the clocking kernels (32..256, step 32;
  * default 256 = 8 warps per SM at 255 registers per thread). */

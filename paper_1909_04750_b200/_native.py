@@ -29,6 +29,8 @@ SYMBOLS = {
     "mk2_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "mk2_destroy": (C.c_int, [_vp]),
     "mk2_set_stream": (C.c_int, [_vp, _vp]),
+    "mk2_use_own_stream": (C.c_int, [_vp]),
+    "mk2_set_chunk_clocks": (C.c_int, [_vp, C.c_uint32]),
     "mk2_sync": (C.c_int, [_vp]),
     "mk2_last_error": (C.c_char_p, [_vp]),
     "mk2_set_group_offset": (C.c_int, [_vp, _u64]),

@@ -29,6 +29,11 @@ struct mk2_ctx {
     uint64_t N = 0, G = 0, cap = 0, g_offset = 0, clocks = 0;
     uint32_t *d_state = nullptr;
     unsigned long long *d_acc = nullptr, *d_sum = nullptr;
+    SchedQueue *d_queue = nullptr;       // persistent-kernel scheduler (mk2_kernels.cuh)
+    unsigned long long *d_slots = nullptr;
+    uint32_t *d_progress = nullptr;
+    uint32_t ring = 0;                   // ring size (power of two >= chains)
+    uint32_t chunk = 4096;               // clocks per scheduling chunk
     void *d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     bool ready = false, async = false, timing_open = false;
@@ -92,11 +97,22 @@ int ensure_capacity(mk2_ctx *ctx, uint64_t G)
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->d_state) cudaFree(ctx->d_state);
     if (ctx->d_acc) cudaFree(ctx->d_acc);
+    if (ctx->d_slots) cudaFree(ctx->d_slots);
+    if (ctx->d_progress) cudaFree(ctx->d_progress);
     ctx->d_state = nullptr;
     ctx->d_acc = nullptr;
+    ctx->d_slots = nullptr;
+    ctx->d_progress = nullptr;
     ctx->cap = 0;
+    const uint64_t chains = (G + 31) / 32;
+    uint64_t ring = 32;
+    while (ring < chains) ring <<= 1;
+    if (ring > 0x80000000ull) return fail(ctx, MK2_E_ARG, "too many instances for one context");
     CK(cudaMalloc(&ctx->d_state, sizeof(uint32_t) * 2 * NBITS * G));
     CK(cudaMalloc(&ctx->d_acc, sizeof(unsigned long long) * G));
+    CK(cudaMalloc(&ctx->d_slots, sizeof(unsigned long long) * ring));
+    CK(cudaMalloc(&ctx->d_progress, sizeof(uint32_t) * chains));
+    ctx->ring = (uint32_t)ring;
     ctx->cap = G;
     return MK2_OK;
 }
@@ -149,10 +165,32 @@ int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bo
     return MK2_OK;
 }
 
+// Persistent launch geometry + scheduler reset for T clocks cut into chunks.
+int launch_sched(mk2_ctx *ctx, uint64_t T, uint32_t chunk, unsigned *grid, uint32_t *cpc)
+{
+    const uint64_t chains = (ctx->G + 31) / 32;
+    const uint64_t n = (T + chunk - 1) / chunk;
+    if (n * chains >= 0xFFFFFFFFull) return fail(ctx, MK2_E_ARG, "too many chunks: raise mk2_set_chunk_clocks");
+    *cpc = (uint32_t)n;
+    const unsigned warps_per_block = (unsigned)ctx->block / 32;
+    const unsigned resident = (unsigned)ctx->sm_count * (unsigned)(BLOCK / ctx->block);
+    *grid = (unsigned)std::min<uint64_t>(resident, (chains + warps_per_block - 1) / warps_per_block);
+    sched_init_kernel<<<(ctx->ring + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_queue, ctx->d_slots, ctx->d_progress,
+                                                                        (uint32_t)chains, *cpc, ctx->ring);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    return MK2_OK;
+}
+
 int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 {
-    gen_colmajor_kernel<<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, stride,
-                                                                       ctx->G, T);
+    unsigned grid;
+    uint32_t cpc;
+    int rc = launch_sched(ctx, T, ctx->chunk, &grid, &cpc);
+    if (rc) return rc;
+    gen_colmajor_kernel<<<grid, ctx->block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, stride, ctx->G, T,
+                                                              ctx->chunk, cpc, ctx->d_queue, ctx->d_slots,
+                                                              ctx->ring - 1, ctx->d_progress);
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -161,12 +199,19 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch)
 {
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
+    const uint32_t chunk = std::max<uint32_t>(128, ctx->chunk / 128 * 128);  // whole 128-clock tiles
+    unsigned grid;
+    uint32_t cpc;
+    int rc = launch_sched(ctx, T, chunk, &grid, &cpc);
+    if (rc) return rc;
     if (aligned)
-        gen_rowmajor_kernel<true><<<blocks_for(ctx->G, ctx->block), ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
-            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T);
+        gen_rowmajor_kernel<true><<<grid, ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
+            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, chunk, cpc, ctx->d_queue, ctx->d_slots,
+            ctx->ring - 1, ctx->d_progress);
     else
-        gen_rowmajor_kernel<false><<<blocks_for(ctx->G, ctx->block), ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
-            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T);
+        gen_rowmajor_kernel<false><<<grid, ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
+            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, chunk, cpc, ctx->d_queue, ctx->d_slots,
+            ctx->ring - 1, ctx->d_progress);
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -243,6 +288,7 @@ int mk2_create(int device, mk2_ctx **out)
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_done[b], cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_sum, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_queue, sizeof(SchedQueue));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM_BYTES);
     if (e == cudaSuccess)
@@ -271,6 +317,9 @@ int mk2_destroy(mk2_ctx *ctx)
     if (ctx->d_state) cudaFree(ctx->d_state);
     if (ctx->d_acc) cudaFree(ctx->d_acc);
     if (ctx->d_sum) cudaFree(ctx->d_sum);
+    if (ctx->d_queue) cudaFree(ctx->d_queue);
+    if (ctx->d_slots) cudaFree(ctx->d_slots);
+    if (ctx->d_progress) cudaFree(ctx->d_progress);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -284,7 +333,24 @@ int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream)
     if (!ctx) return MK2_E_ARG;
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own;
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);  // 0 is a real stream: the legacy default stream
+    return MK2_OK;
+}
+
+int mk2_use_own_stream(mk2_ctx *ctx)
+{
+    if (!ctx) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = ctx->own;
+    return MK2_OK;
+}
+
+int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (clocks < 128) return fail(ctx, MK2_E_ARG, "chunk must be at least 128 clocks");
+    ctx->chunk = clocks;
     return MK2_OK;
 }
 

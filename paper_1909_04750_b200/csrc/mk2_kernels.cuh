@@ -249,52 +249,153 @@ __device__ __forceinline__ void acc_add(unsigned long long &acc, uint32_t z)
 }
 
 // ---------------------------------------------------------------------------
+// Persistent scheduling of the keystream kernels.
+//
+// A "chain" is one warp's worth of groups (32 threads x 32 instances = 1024
+// instances); its clocks are strictly serial, chains are independent.  The
+// keystream of a chain is cut into chunks of `chunk` clocks.  Worker warps (one
+// persistent CTA per SM) pull READY chains from a device-side FIFO ring, run one
+// chunk (state in registers), park the state in HBM and push the chain back.
+// With fewer chains than resident warps x sub-partition capacity (BASELINE
+// config 2: 1024 chains on 592 sub-partitions) a static launch idles 14% of the
+// ALU pipes; the FIFO hands a finished chain to the longest-idle worker, so
+// load follows free sub-partitions.  With many chains it is a plain dynamic
+// tile scheduler with a short tail.
+//
+// Ring entry = (ticket + 1) << 32 | chain, written with one 64-bit store, so a
+// consumer spinning on its ticket's slot needs no separate flag.  State handed
+// between SMs goes through L2 (ld.cg / st.cg + __threadfence on both sides).
+// ---------------------------------------------------------------------------
+struct SchedQueue {
+    unsigned long long head;        // next pop ticket
+    unsigned long long tail;        // next push ticket
+    unsigned long long total_jobs;  // chains * chunks_per_chain
+    unsigned long long pad;
+};
+
+__global__ void sched_init_kernel(SchedQueue *q, unsigned long long *slots, uint32_t *progress, uint32_t chains,
+                                  uint32_t chunks_per_chain, uint32_t ring)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        q->head = 0ull;
+        q->tail = chains;
+        q->total_jobs = (unsigned long long)chains * chunks_per_chain;
+    }
+    // tickets 0..chains-1 are pre-filled; every other slot is cleared so that an
+    // entry left by an earlier launch can never match a ticket of this one
+    if (i < ring) slots[i] = i < chains ? (((unsigned long long)(i + 1) << 32) | i) : 0ull;
+    if (i < chains) progress[i] = 0u;
+}
+
+// Returns false when all work has been handed out.  Warp-uniform.
+__device__ __forceinline__ bool sched_pop(SchedQueue *q, const unsigned long long *slots, uint32_t mask,
+                                          uint32_t &chain)
+{
+    const unsigned lane = threadIdx.x & 31u;
+    unsigned long long e = 0ull;
+    if (lane == 0) {
+        const unsigned long long t = atomicAdd(&q->head, 1ull);
+        if (t >= *reinterpret_cast<volatile unsigned long long *>(&q->total_jobs)) {
+            e = ~0ull;
+        } else {
+            const volatile unsigned long long *slot = slots + (t & mask);
+            while (((e = *slot) >> 32) != ((t + 1) & 0xFFFFFFFFull)) __nanosleep(64);
+        }
+    }
+    e = __shfl_sync(0xFFFFFFFFu, e, 0);
+    __threadfence();  // acquire: the chain's parked state is visible after its ring entry
+    chain = (uint32_t)e;
+    return e != ~0ull;
+}
+
+// All lanes have written the chain's state back.  Warp-uniform call.
+__device__ __forceinline__ void sched_push(SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress,
+                                           uint32_t chain, uint32_t k_done, uint32_t chunks_per_chain)
+{
+    __threadfence();  // release this lane's state stores
+    __syncwarp();
+    if ((threadIdx.x & 31u) == 0) {
+        __stcg(progress + chain, k_done);
+        if (k_done < chunks_per_chain) {
+            __threadfence();
+            const unsigned long long t = atomicAdd(&q->tail, 1ull);
+            *reinterpret_cast<volatile unsigned long long *>(slots + (t & mask)) = ((t + 1) << 32) | chain;
+        }
+    }
+}
+
+__device__ __forceinline__ void load_state(const uint32_t *__restrict__ state, uint64_t G, uint64_t g,
+                                           uint32_t (&r)[NBITS], uint32_t (&s)[NBITS])
+{
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        r[i] = __ldcg(state + (uint64_t)i * G + g);
+        s[i] = __ldcg(state + (uint64_t)(NBITS + i) * G + g);
+    }
+}
+__device__ __forceinline__ void store_state(uint32_t *__restrict__ state, uint64_t G, uint64_t g,
+                                            const uint32_t (&r)[NBITS], const uint32_t (&s)[NBITS])
+{
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        __stcg(state + (uint64_t)i * G + g, r[i]);
+        __stcg(state + (uint64_t)(NBITS + i) * G + g, s[i]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Keystream, column-major: out[t * stride + g] = z_t (mickey.py:362-368; the
 // compiled loop kernels.py:46-95).  Resumable: state and the checksum
-// accumulator are loaded and stored back.
+// accumulator live in HBM between chunks and between calls.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(BLOCK, 1)
 gen_colmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc,
-                    uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T)
+                    uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T, uint32_t chunk,
+                    uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots, uint32_t mask,
+                    uint32_t *progress)
 {
-    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (g >= G) return;
-    uint32_t r[NBITS], s[NBITS];
-#pragma unroll
-    for (int i = 0; i < NBITS; ++i) {
-        r[i] = state[(uint64_t)i * G + g];
-        s[i] = state[(uint64_t)(NBITS + i) * G + g];
-    }
-    unsigned long long a = acc[g];
-    uint32_t *p = out + g;
+    uint32_t chain;
+    while (sched_pop(q, slots, mask, chain)) {
+        const uint32_t k = __ldcg(progress + chain);
+        const uint64_t g = (uint64_t)chain * 32 + (threadIdx.x & 31u);
+        const uint64_t t0 = (uint64_t)k * chunk;
+        const uint64_t tc = T - t0 < chunk ? T - t0 : chunk;
+        if (g < G) {
+            uint32_t r[NBITS], s[NBITS];
+            load_state(state, G, g, r, s);
+            unsigned long long a = __ldcg(acc + g);
+            uint32_t *p = out + t0 * stride + g;
 #pragma unroll 1
-    for (uint64_t t = 0; t < T; ++t) {
-        const uint32_t z = keystream_word(r, s);
-        *p = z;
-        p += stride;
-        acc_add(a, z);
-        clock<false, false>(r, s, 0u);
+            for (uint64_t t = 0; t < tc; ++t) {
+                const uint32_t z = keystream_word(r, s);
+                *p = z;
+                p += stride;
+                acc_add(a, z);
+                clock<false, false>(r, s, 0u);
+            }
+            store_state(state, G, g, r, s);
+            __stcg(acc + g, a);
+        }
+        sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }
-#pragma unroll
-    for (int i = 0; i < NBITS; ++i) {
-        state[(uint64_t)i * G + g] = r[i];
-        state[(uint64_t)(NBITS + i) * G + g] = s[i];
-    }
-    acc[g] = a;
 }
 
 // ---------------------------------------------------------------------------
 // Keystream, row-major: out[(32 g + j) * pitch + t / 8], MSB-first bytes
 // (kernels.py:604-621, bitops.py:20-23).
 //
-// Every 8 clocks the thread transposes its 8 keystream words (8 x 32 bits) in
-// registers into 32 output bytes (word k, byte q = instance 8q + k), and parks
-// the 8 words in its private shared-memory column (conflict-free: the word
-// index varies with tid).  After 16 such groups (128 clocks) it reads them
-// back per k, regroups bytes -> words with PRMT (4x4 byte transposes) and
-// issues one 16-byte store per instance row.  Shared memory is only a register
-// extension here (the 200 state words leave no room for 128 more), each thread
-// reads back only what it wrote, so no barrier is needed.
+// The clock loop is the same one-clock body as above, except that z_t goes to
+// the thread's private shared-memory column (tile[t % 128][tid], conflict-free)
+// instead of HBM: the 200 state words leave no registers to hold keystream.
+// Every 128 clocks the thread drains its column in two small loops:
+//   pass 1  per 8 clocks: 8 words back into registers, 8x32 bit transpose
+//           (word k, byte q = the output byte of instance 8q + k), back to smem;
+//   pass 2  per k: 16 words (one per 8-clock group) -> 4x4 byte transposes with
+//           PRMT -> one 16-byte store per instance row.
+// Each thread only ever reads what it wrote, so no barrier is needed; the code
+// stays small enough for the instruction cache (an 8-clock unrolled body is
+// 43 KB and measurably starves instruction fetch).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
 {
@@ -318,77 +419,85 @@ __device__ __forceinline__ void bytes4x4(const uint32_t (&x)[4], uint32_t (&y)[4
 template <bool ALIGNED16>
 __global__ void __launch_bounds__(BLOCK, 1)
 gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc, uint8_t *__restrict__ out,
-                    uint64_t pitch, uint64_t N, uint64_t G, uint64_t T)
+                    uint64_t pitch, uint64_t N, uint64_t G, uint64_t T, uint32_t chunk, uint32_t chunks_per_chain,
+                    SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress)
 {
-    extern __shared__ uint32_t tile[];  // [8 k][ROW_GROUPS][BLOCK]
-    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (g >= G) return;
-    uint32_t r[NBITS], s[NBITS];
-#pragma unroll
-    for (int i = 0; i < NBITS; ++i) {
-        r[i] = state[(uint64_t)i * G + g];
-        s[i] = state[(uint64_t)(NBITS + i) * G + g];
-    }
-    unsigned long long a = acc[g];
+    extern __shared__ uint32_t tile[];  // [8 * ROW_GROUPS clocks][BLOCK]
     uint32_t *col = tile + threadIdx.x;
-    uint8_t *rows = out + 32 * g * pitch;
-    const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;  // rows of this group that exist
+    uint32_t chain;
+    while (sched_pop(q, slots, mask, chain)) {
+        const uint32_t k = __ldcg(progress + chain);
+        const uint64_t g = (uint64_t)chain * 32 + (threadIdx.x & 31u);
+        const uint64_t c0 = (uint64_t)k * chunk;  // chunk is a multiple of 128 clocks
+        const uint64_t tc = T - c0 < chunk ? T - c0 : chunk;
+        if (g < G) {
+            uint32_t r[NBITS], s[NBITS];
+            load_state(state, G, g, r, s);
+            unsigned long long a = __ldcg(acc + g);
+            uint8_t *rows = out + 32 * g * pitch + (c0 >> 3);
+            const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;  // rows of this group that exist
 
 #pragma unroll 1
-    for (uint64_t t0 = 0; t0 < T; t0 += 8 * ROW_GROUPS) {
-        const int ngrp = (T - t0) >= 8 * ROW_GROUPS ? ROW_GROUPS : (int)((T - t0) >> 3);
+            for (uint64_t t0 = 0; t0 < tc; t0 += 8 * ROW_GROUPS) {
+                const int nclk = (tc - t0) >= 8 * ROW_GROUPS ? 8 * ROW_GROUPS : (int)(tc - t0);
+                const int ngrp = nclk >> 3;
+                uint32_t *zp = col;
 #pragma unroll 1
-        for (int grp = 0; grp < ngrp; ++grp) {
-            uint32_t z[8];
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const uint32_t zz = keystream_word(r, s);
-                z[7 - m] = zz;  // clock t0 + 8 grp + m lands in bit 7 - m of the byte (MSB-first)
-                acc_add(a, zz);
-                clock<false, false>(r, s, 0u);
-            }
-            transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
-#pragma unroll
-            for (int k = 0; k < 8; ++k) col[(k * ROW_GROUPS + grp) * BLOCK] = z[k];
-        }
-        // ---- drain: 16 bytes (or the tail) per instance row
-        uint8_t *dst = rows + (t0 >> 3);
-        if (ALIGNED16 && ngrp == ROW_GROUPS && nrows == 32) {
-#pragma unroll 2
-            for (int k = 0; k < 8; ++k) {
-                uint32_t y[4][4];  // [g4][q]
-#pragma unroll
-                for (int g4 = 0; g4 < 4; ++g4) {
-                    uint32_t x[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) x[u] = col[(k * ROW_GROUPS + 4 * g4 + u) * BLOCK];
-                    bytes4x4(x, y[g4]);
+                for (int t = 0; t < nclk; ++t) {
+                    const uint32_t z = keystream_word(r, s);
+                    *zp = z;
+                    zp += BLOCK;
+                    acc_add(a, z);
+                    clock<false, false>(r, s, 0u);
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * q + k) * pitch) =
-                        make_uint4(y[0][q], y[1][q], y[2][q], y[3][q]);
-            }
-        } else {
-            // ragged edge: short tail, partial last group or unaligned rows
-#pragma unroll 1
-            for (int k = 0; k < 8; ++k)
+                // ---- pass 1: bit transposes, in place in the smem column
 #pragma unroll 1
                 for (int grp = 0; grp < ngrp; ++grp) {
-                    const uint32_t x = col[(k * ROW_GROUPS + grp) * BLOCK];
+                    uint32_t z[8];
+                    uint32_t *gp = col + grp * 8 * BLOCK;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if ((uint64_t)(8 * q + k) < nrows)
-                            dst[(uint64_t)(8 * q + k) * pitch + grp] = (uint8_t)(x >> (8 * q));
+                    for (int m = 0; m < 8; ++m) z[7 - m] = gp[m * BLOCK];  // clock m -> bit 7 - m (MSB-first)
+                    transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) gp[kk * BLOCK] = z[kk];
                 }
-        }
-    }
+                // ---- pass 2: 16 bytes (or the tail) per instance row
+                uint8_t *dst = rows + (t0 >> 3);
+                if (ALIGNED16 && ngrp == ROW_GROUPS && nrows == 32) {
+#pragma unroll 1
+                    for (int kk = 0; kk < 8; ++kk) {
+                        uint32_t y[4][4];  // [g4][q]
 #pragma unroll
-    for (int i = 0; i < NBITS; ++i) {
-        state[(uint64_t)i * G + g] = r[i];
-        state[(uint64_t)(NBITS + i) * G + g] = s[i];
+                        for (int g4 = 0; g4 < 4; ++g4) {
+                            uint32_t x[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) x[u] = col[((4 * g4 + u) * 8 + kk) * BLOCK];
+                            bytes4x4(x, y[g4]);
+                        }
+#pragma unroll
+                        for (int qq = 0; qq < 4; ++qq)
+                            __stcs(reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch),
+                                   make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]));
+                    }
+                } else {
+                    // ragged edge: short tail, partial last group or unaligned rows
+#pragma unroll 1
+                    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll 1
+                        for (int grp = 0; grp < ngrp; ++grp) {
+                            const uint32_t x = col[(grp * 8 + kk) * BLOCK];
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                if ((uint64_t)(8 * qq + kk) < nrows)
+                                    dst[(uint64_t)(8 * qq + kk) * pitch + grp] = (uint8_t)(x >> (8 * qq));
+                        }
+                }
+            }
+            store_state(state, G, g, r, s);
+            __stcg(acc + g, a);
+        }
+        sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }
-    acc[g] = a;
 }
 
 // ---------------------------------------------------------------------------

@@ -74,8 +74,16 @@ class MickeyGenerator:
         check(rc, self._ctx, what)
 
     def set_stream(self, cuda_stream: Optional[int]):
-        """Launch on an external CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
-        self._ck(self._lib.mk2_set_stream(self._ctx, C.c_void_p(cuda_stream or 0)), "mk2_set_stream")
+        """Launch on an external CUDA stream handle (e.g. torch.cuda.current_stream().cuda_stream;
+        0 is the legacy default stream).  None goes back to the context's own stream."""
+        if cuda_stream is None:
+            self._ck(self._lib.mk2_use_own_stream(self._ctx), "mk2_use_own_stream")
+        else:
+            self._ck(self._lib.mk2_set_stream(self._ctx, C.c_void_p(int(cuda_stream))), "mk2_set_stream")
+
+    def set_chunk_clocks(self, clocks: int):
+        """Tuning knob: clocks per scheduling chunk of the persistent keystream kernels."""
+        self._ck(self._lib.mk2_set_chunk_clocks(self._ctx, int(clocks)), "mk2_set_chunk_clocks")
 
     def set_async(self, flag: bool):
         self._ck(self._lib.mk2_set_async(self._ctx, int(bool(flag))), "mk2_set_async")

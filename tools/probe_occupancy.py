@@ -19,18 +19,16 @@ sms = torch.cuda.get_device_properties(0).multi_processor_count
 print(json.dumps({"lop3_peak_Tlaneops": peak / 1e12, "probe_ms": ms, "sms": sms,
                   "implied_lanes_per_clk_per_sm_at_1965MHz": peak / sms / 1.965e9}))
 configs = []
-for block in (128, 256):
-    for warps_per_sm in (4, 8):
-        if warps_per_sm * 32 < block:
-            continue
-        G = sms * warps_per_sm * 32
-        configs.append((block, G, f"{warps_per_sm} warps/SM"))
-    configs.append((block, 32768, "C2 geometry (2^20 instances)"))
-    configs.append((block, 1 << 19, "C3 geometry (2^24 instances)"))
+for block, chunk in ((256, 1 << 30), (256, 8192), (256, 4096), (256, 2048), (256, 1024), (128, 4096), (128, 1024)):
+    configs.append((block, chunk, sms * 8 * 32, "8 warps/SM exactly"))
+    configs.append((block, chunk, 32768, "C2 geometry (2^20 instances)"))
+    if chunk in (1 << 30, 4096):
+        configs.append((block, chunk, 1 << 19, "C3 geometry (2^24 instances)"))
 for layout in ("col", "row"):
-    for block, G, label in configs:
+    for block, chunk, G, label in configs:
         n = G * 32
         gen.set_block_threads(block)
+        gen.set_chunk_clocks(chunk)
         gen.init_counter(KEY, 0, n)
         if layout == "col":
             out = torch.empty((T, G), dtype=torch.int32, device="cuda")
@@ -44,7 +42,7 @@ for layout in ("col", "row"):
             fn()
             best = min(best, gen.last_kernel_ms)
         ops = n * T * 327 / 32
-        print(json.dumps({"layout": layout, "block": block, "G": G, "label": label, "T": T, "ms": round(best, 3),
+        print(json.dumps({"layout": layout, "block": block, "chunk": chunk, "G": G, "label": label, "T": T, "ms": round(best, 3),
                           "Tbps": round(n * T / best / 1e9, 4), "lop3_frac": round(ops / (best * 1e-3) / peak, 4)}))
         del out
 gen.close()
