@@ -152,12 +152,24 @@ int mk2_last_kernel_launches(const mk2_ctx *ctx);
 int mk2_set_async(mk2_ctx *ctx, int async);
 
 /* Tuning knob: clocks per scheduling chunk of the persistent keystream kernels
- * (>= 128, default 4096): a chain of 1024 instances runs one chunk, parks its
- * state and goes back to the ready queue. */
+ * (0 = automatic, else >= 128): a chain of 1024 instances runs one chunk, parks
+ * its state and goes back to the ready queue.
+ * mk2_last_plan reports what the most recent keystream launch used. */
 int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
+int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 
-/* Tuning knob: threads per CTA of the clocking kernels (32..256, step 32;
- * default 256 = 8 warps per SM at 255 registers per thread). */
+/* Diagnostics: per-job trace of the column-major persistent kernel.  Records
+ * are 48-byte structs {u32 chain, k, smid, warp; u64 t_pop, t_start, t_end
+ * (ns, %globaltimer); u64 pad}.  capacity 0 switches tracing off.
+ * mk2_read_trace copies out and clears the records gathered so far.
+ * mk2_set_max_ctas caps the number of persistent CTAs (0 = no cap). */
+int mk2_set_trace(mk2_ctx *ctx, uint64_t capacity);
+int mk2_read_trace(mk2_ctx *ctx, void *records, uint64_t max_records, uint64_t *count);
+int mk2_set_max_ctas(mk2_ctx *ctx, uint32_t ctas);
+
+/* Tuning knob: threads per persistent CTA of the keystream kernels (0 =
+ * automatic; else 32..256 in steps of 32; one CTA per SM, 255 registers per
+ * thread, so 128 = one worker warp per SM sub-partition, 256 = two). */
 int mk2_set_block_threads(mk2_ctx *ctx, int threads);
 
 /*

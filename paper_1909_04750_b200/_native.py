@@ -31,6 +31,7 @@ SYMBOLS = {
     "mk2_set_stream": (C.c_int, [_vp, _vp]),
     "mk2_use_own_stream": (C.c_int, [_vp]),
     "mk2_set_chunk_clocks": (C.c_int, [_vp, C.c_uint32]),
+    "mk2_last_plan": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_uint32)]),
     "mk2_sync": (C.c_int, [_vp]),
     "mk2_last_error": (C.c_char_p, [_vp]),
     "mk2_set_group_offset": (C.c_int, [_vp, _u64]),
@@ -48,6 +49,9 @@ SYMBOLS = {
     "mk2_last_kernel_launches": (C.c_int, [_vp]),
     "mk2_set_async": (C.c_int, [_vp, C.c_int]),
     "mk2_set_block_threads": (C.c_int, [_vp, C.c_int]),
+    "mk2_set_trace": (C.c_int, [_vp, _u64]),
+    "mk2_read_trace": (C.c_int, [_vp, _vp, _u64, C.POINTER(_u64)]),
+    "mk2_set_max_ctas": (C.c_int, [_vp, C.c_uint32]),
     "mk2_lop3_peak": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
     "mk2_lop3_per_clock": (C.c_int, []),
 }

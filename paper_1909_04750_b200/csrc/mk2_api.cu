@@ -33,7 +33,12 @@ struct mk2_ctx {
     unsigned long long *d_slots = nullptr;
     uint32_t *d_progress = nullptr;
     uint32_t ring = 0;                   // ring size (power of two >= chains)
-    uint32_t chunk = 4096;               // clocks per scheduling chunk
+    uint32_t chunk_user = 0;             // user override of clocks per scheduling chunk (0 = automatic)
+    int block_user = 0;                  // user override of threads per persistent CTA (0 = automatic)
+    int last_plan_block = 0;
+    uint32_t last_plan_chunk = 0;
+    Trace trace = {nullptr, nullptr, 0}; // optional per-job trace (device buffers owned by the ctx)
+    unsigned max_grid = 0;               // debug knob: cap on persistent CTAs (0 = one per SM slot)
     void *d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     bool ready = false, async = false, timing_open = false;
@@ -105,8 +110,8 @@ int ensure_capacity(mk2_ctx *ctx, uint64_t G)
     ctx->d_progress = nullptr;
     ctx->cap = 0;
     const uint64_t chains = (G + 31) / 32;
-    uint64_t ring = 32;
-    while (ring < chains) ring <<= 1;
+    uint64_t ring = 64;  // power of two >= 2 x chains: a slot is never rewritten while its reader may still poll it
+    while (ring < 2 * chains) ring <<= 1;
     if (ring > 0x80000000ull) return fail(ctx, MK2_E_ARG, "too many instances for one context");
     CK(cudaMalloc(&ctx->d_state, sizeof(uint32_t) * 2 * NBITS * G));
     CK(cudaMalloc(&ctx->d_acc, sizeof(unsigned long long) * G));
@@ -165,32 +170,93 @@ int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bo
     return MK2_OK;
 }
 
-// Persistent launch geometry + scheduler reset for T clocks cut into chunks.
-int launch_sched(mk2_ctx *ctx, uint64_t T, uint32_t chunk, unsigned *grid, uint32_t *cpc)
+// ---------------------------------------------------------------------------
+// Schedule of one keystream launch: how many worker warps per SM and how the T
+// clocks of every chain (= 1024 instances) are cut into chunks.
+//
+// Measured on B200 (profiles/): one warp alone on an SM sub-partition already
+// runs the clock loop at 98.9% of the LOP3 issue rate, two warps share it at
+// 99.1%, and parking / reloading a chain's state costs nothing measurable even
+// for 512-clock chunks.  So:
+//   * plenty of chains (>= 2 x 8 warps x SMs): 8 worker warps per SM, fixed
+//     chunk; the FIFO is a dynamic tile scheduler with a short tail;
+//   * fewer chains (BASELINE config 2: 1024 chains, 592 sub-partitions): one
+//     worker warp per sub-partition and the chunk COUNT K chosen so that
+//     chains x K is as close as possible below a multiple of the worker count
+//     (1024 x 37 = 592 x 64): every sub-partition stays busy to the end
+//     instead of 1024 warps sitting unevenly on 592 sub-partitions (-14%).
+// mk2_set_block_threads / mk2_set_chunk_clocks override the automatic choice.
+// ---------------------------------------------------------------------------
+struct Plan {
+    int block;        // threads per CTA (4 or 8 worker warps), one CTA per SM
+    uint32_t chunk;   // clocks per chunk
+    uint32_t cpc;     // chunks per chain
+    unsigned grid;
+};
+
+Plan make_plan(const mk2_ctx *ctx, uint64_t T, uint32_t granule)
 {
     const uint64_t chains = (ctx->G + 31) / 32;
-    const uint64_t n = (T + chunk - 1) / chunk;
-    if (n * chains >= 0xFFFFFFFFull) return fail(ctx, MK2_E_ARG, "too many chunks: raise mk2_set_chunk_clocks");
-    *cpc = (uint32_t)n;
-    const unsigned warps_per_block = (unsigned)ctx->block / 32;
-    const unsigned resident = (unsigned)ctx->sm_count * (unsigned)(BLOCK / ctx->block);
-    *grid = (unsigned)std::min<uint64_t>(resident, (chains + warps_per_block - 1) / warps_per_block);
+    const uint64_t sms = (uint64_t)ctx->sm_count;
+    Plan p{};
+    auto round_chunk = [&](uint64_t c) {
+        c = std::max<uint64_t>(c, granule);
+        c = (c + granule - 1) / granule * granule;
+        return (uint32_t)std::min<uint64_t>(c, 0x7FFFFF80ull);
+    };
+    p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? 256 : 128);
+    const uint64_t workers = sms * (uint64_t)(p.block / 32);
+    if (ctx->chunk_user) {
+        p.chunk = round_chunk(ctx->chunk_user);
+    } else if (chains >= 2 * workers || chains <= workers) {
+        p.chunk = round_chunk(std::min<uint64_t>(T, chains <= workers ? T : 4096));
+    } else {
+        // workers < chains < 2 x workers: pick K for the least idle time in the last round
+        const uint64_t kmax = std::max<uint64_t>(1, std::min<uint64_t>(128, T / 1024));
+        double best = 1e30;
+        uint64_t best_k = 1;
+        for (uint64_t k = 1; k <= kmax; ++k) {
+            const uint32_t c = round_chunk((T + k - 1) / k);
+            const uint64_t keff = (T + c - 1) / c;
+            const uint64_t jobs = chains * keff;
+            const double rounds = (double)((jobs + workers - 1) / workers);
+            const double cost = rounds * c;  // time ~ rounds x chunk length
+            if (cost < best * 0.998) {
+                best = cost;
+                best_k = k;
+            }
+        }
+        p.chunk = round_chunk((T + best_k - 1) / best_k);
+    }
+    p.cpc = (uint32_t)((T + p.chunk - 1) / p.chunk);
+    p.grid = (unsigned)std::min<uint64_t>(sms, (chains + p.block / 32 - 1) / (p.block / 32));
+    if (chains > workers) p.grid = (unsigned)sms;
+    if (ctx->max_grid) p.grid = std::min(p.grid, ctx->max_grid);
+    return p;
+}
+
+// Scheduler reset for one launch.
+int launch_sched(mk2_ctx *ctx, const Plan &p)
+{
+    const uint64_t chains = (ctx->G + 31) / 32;
+    if ((uint64_t)p.cpc * chains >= 0xFFFFFFFFull) return fail(ctx, MK2_E_ARG, "too many chunks: raise mk2_set_chunk_clocks");
     sched_init_kernel<<<(ctx->ring + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_queue, ctx->d_slots, ctx->d_progress,
-                                                                        (uint32_t)chains, *cpc, ctx->ring);
+                                                                        (uint32_t)chains, p.cpc, ctx->ring);
     CK(cudaGetLastError());
     ctx->last_launches++;
+    ctx->last_plan_block = p.block;
+    ctx->last_plan_chunk = p.chunk;
     return MK2_OK;
 }
 
 int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 {
-    unsigned grid;
-    uint32_t cpc;
-    int rc = launch_sched(ctx, T, ctx->chunk, &grid, &cpc);
+    const Plan p = make_plan(ctx, T, 1);
+    int rc = launch_sched(ctx, p);
     if (rc) return rc;
-    gen_colmajor_kernel<<<grid, ctx->block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, stride, ctx->G, T,
-                                                              ctx->chunk, cpc, ctx->d_queue, ctx->d_slots,
-                                                              ctx->ring - 1, ctx->d_progress);
+    gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out,
+                                                             stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                                                             ctx->d_slots, ctx->ring - 1, ctx->d_progress, ctx->trace);
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -199,19 +265,17 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch)
 {
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
-    const uint32_t chunk = std::max<uint32_t>(128, ctx->chunk / 128 * 128);  // whole 128-clock tiles
-    unsigned grid;
-    uint32_t cpc;
-    int rc = launch_sched(ctx, T, chunk, &grid, &cpc);
+    const Plan p = make_plan(ctx, T, 8 * ROW_GROUPS);  // whole 128-clock tiles
+    int rc = launch_sched(ctx, p);
     if (rc) return rc;
     if (aligned)
-        gen_rowmajor_kernel<true><<<grid, ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
-            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, chunk, cpc, ctx->d_queue, ctx->d_slots,
-            ctx->ring - 1, ctx->d_progress);
+        gen_rowmajor_kernel<true><<<p.grid, p.block, ROW_SMEM_BYTES, ctx->stream>>>(
+            ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
+            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress);
     else
-        gen_rowmajor_kernel<false><<<grid, ctx->block, ROW_SMEM_BYTES, ctx->stream>>>(
-            ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, chunk, cpc, ctx->d_queue, ctx->d_slots,
-            ctx->ring - 1, ctx->d_progress);
+        gen_rowmajor_kernel<false><<<p.grid, p.block, ROW_SMEM_BYTES, ctx->stream>>>(
+            ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
+            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress);
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -318,6 +382,8 @@ int mk2_destroy(mk2_ctx *ctx)
     if (ctx->d_acc) cudaFree(ctx->d_acc);
     if (ctx->d_sum) cudaFree(ctx->d_sum);
     if (ctx->d_queue) cudaFree(ctx->d_queue);
+    if (ctx->trace.rec) cudaFree(ctx->trace.rec);
+    if (ctx->trace.count) cudaFree(ctx->trace.count);
     if (ctx->d_slots) cudaFree(ctx->d_slots);
     if (ctx->d_progress) cudaFree(ctx->d_progress);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -346,19 +412,71 @@ int mk2_use_own_stream(mk2_ctx *ctx)
     return MK2_OK;
 }
 
+int mk2_set_trace(mk2_ctx *ctx, uint64_t capacity)
+{
+    if (!ctx) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->trace.rec) cudaFree(ctx->trace.rec);
+    if (ctx->trace.count) cudaFree(ctx->trace.count);
+    ctx->trace = {nullptr, nullptr, 0};
+    if (capacity) {
+        CK(cudaMalloc(&ctx->trace.rec, sizeof(TraceRec) * capacity));
+        CK(cudaMalloc(&ctx->trace.count, sizeof(unsigned long long)));
+        CK(cudaMemset(ctx->trace.count, 0, sizeof(unsigned long long)));
+        ctx->trace.capacity = capacity;
+    }
+    return MK2_OK;
+}
+
+int mk2_read_trace(mk2_ctx *ctx, void *records, uint64_t max_records, uint64_t *count)
+{
+    if (!ctx || !count) return MK2_E_ARG;
+    *count = 0;
+    if (!ctx->trace.rec) return MK2_OK;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    unsigned long long n = 0;
+    CK(cudaMemcpy(&n, ctx->trace.count, sizeof n, cudaMemcpyDeviceToHost));
+    n = std::min<unsigned long long>(n, std::min<unsigned long long>(ctx->trace.capacity, max_records));
+    if (n && records) CK(cudaMemcpy(records, ctx->trace.rec, sizeof(TraceRec) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->trace.count, 0, sizeof(unsigned long long)));
+    *count = n;
+    return MK2_OK;
+}
+
+int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (block_threads) *block_threads = ctx->last_plan_block;
+    if (chunk_clocks) *chunk_clocks = ctx->last_plan_chunk;
+    return MK2_OK;
+}
+
+int mk2_set_max_ctas(mk2_ctx *ctx, uint32_t ctas)
+{
+    if (!ctx) return MK2_E_ARG;
+    ctx->max_grid = ctas;
+    return MK2_OK;
+}
+
 int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
 {
     if (!ctx) return MK2_E_ARG;
-    if (clocks < 128) return fail(ctx, MK2_E_ARG, "chunk must be at least 128 clocks");
-    ctx->chunk = clocks;
+    if (clocks != 0 && clocks < 128) return fail(ctx, MK2_E_ARG, "chunk must be 0 (auto) or at least 128 clocks");
+    ctx->chunk_user = clocks;
     return MK2_OK;
 }
 
 int mk2_set_block_threads(mk2_ctx *ctx, int threads)
 {
     if (!ctx) return MK2_E_ARG;
-    if (threads < 32 || threads > BLOCK || threads % 32) return fail(ctx, MK2_E_ARG, "threads per CTA must be 32..256 in steps of 32");
-    ctx->block = threads;
+    if (threads == 0) {
+        ctx->block_user = 0;
+        return MK2_OK;
+    }
+    if (threads < 32 || threads > BLOCK || threads % 32) return fail(ctx, MK2_E_ARG, "threads per CTA must be 0 (auto) or 32..256 in steps of 32");
+    ctx->block_user = threads;
     return MK2_OK;
 }
 

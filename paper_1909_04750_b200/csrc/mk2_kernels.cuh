@@ -273,11 +273,50 @@ struct SchedQueue {
     unsigned long long pad;
 };
 
+// Optional per-job trace (mk2_set_trace): who ran which chunk where and when.
+struct TraceRec {
+    uint32_t chain, k, smid, warp;
+    unsigned long long t_pop, t_start, t_end;  // %globaltimer, ns
+    unsigned long long pad;
+};
+struct Trace {
+    TraceRec *rec;
+    unsigned long long *count;
+    unsigned long long capacity;
+};
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid()
+{
+    uint32_t v;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+    return v;
+}
+__device__ __forceinline__ void trace_job(const Trace &tr, uint32_t chain, uint32_t k, unsigned long long t_pop,
+                                          unsigned long long t_start)
+{
+    if (tr.rec && (threadIdx.x & 31u) == 0) {
+        const unsigned long long i = atomicAdd(tr.count, 1ull);
+        if (i < tr.capacity) {
+            TraceRec r;
+            r.chain = chain; r.k = k; r.smid = smid(); r.warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+            r.t_pop = t_pop; r.t_start = t_start; r.t_end = gtime(); r.pad = 0;
+            tr.rec[i] = r;
+        }
+    }
+    __syncwarp();
+}
+
 __global__ void sched_init_kernel(SchedQueue *q, unsigned long long *slots, uint32_t *progress, uint32_t chains,
                                   uint32_t chunks_per_chain, uint32_t ring)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {
+        q->pad = 0ull;
         q->head = 0ull;
         q->tail = chains;
         q->total_jobs = (unsigned long long)chains * chunks_per_chain;
@@ -288,60 +327,110 @@ __global__ void sched_init_kernel(SchedQueue *q, unsigned long long *slots, uint
     if (i < chains) progress[i] = 0u;
 }
 
-// Returns false when all work has been handed out.  Warp-uniform.
+// Memory-ordering helpers (PTX memory model, gpu scope).  st.release compiles to
+// MEMBAR.ALL.GPU + a strong store and, unlike __threadfence(), does not
+// invalidate L1; ld.acquire is a strong load followed by one L1 invalidate.
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Returns false when all work has been handed out.  The whole warp executes
+// every instruction here (lane 0's atomic is predicated, the poll is one
+// broadcast load): a lane-0-only polling loop was measured to leave the warp
+// running its next job at half speed.
 __device__ __forceinline__ bool sched_pop(SchedQueue *q, const unsigned long long *slots, uint32_t mask,
                                           uint32_t &chain)
 {
     const unsigned lane = threadIdx.x & 31u;
-    unsigned long long e = 0ull;
-    if (lane == 0) {
-        const unsigned long long t = atomicAdd(&q->head, 1ull);
-        if (t >= *reinterpret_cast<volatile unsigned long long *>(&q->total_jobs)) {
-            e = ~0ull;
-        } else {
-            const volatile unsigned long long *slot = slots + (t & mask);
-            while (((e = *slot) >> 32) != ((t + 1) & 0xFFFFFFFFull)) __nanosleep(64);
-        }
+    unsigned long long t = 0ull;
+    if (lane == 0) t = atomicAdd(&q->head, 1ull);
+    t = __shfl_sync(0xFFFFFFFFu, t, 0);
+    if (t >= ld_relaxed_u64(&q->total_jobs)) return false;
+    const unsigned long long *slot = slots + (t & mask);
+    const unsigned long long want = (t + 1) & 0xFFFFFFFFull;
+    unsigned ns = 32;
+    while ((ld_relaxed_u64(slot) >> 32) != want) {
+        __nanosleep(ns);
+        if (ns < 512) ns <<= 1;
     }
-    e = __shfl_sync(0xFFFFFFFFu, e, 0);
-    __threadfence();  // acquire: the chain's parked state is visible after its ring entry
-    chain = (uint32_t)e;
-    return e != ~0ull;
+    const unsigned long long e = ld_acquire_u64(slot);  // acquire: the chain's parked state is visible
+    chain = (uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)e, 0);
+    return true;
 }
 
-// All lanes have written the chain's state back.  Warp-uniform call.
+// Every lane has already published its share of the chain's state with a
+// release store (store_state); lane 0 hands the chain to the next worker.
 __device__ __forceinline__ void sched_push(SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress,
                                            uint32_t chain, uint32_t k_done, uint32_t chunks_per_chain)
 {
-    __threadfence();  // release this lane's state stores
     __syncwarp();
     if ((threadIdx.x & 31u) == 0) {
         __stcg(progress + chain, k_done);
         if (k_done < chunks_per_chain) {
-            __threadfence();
             const unsigned long long t = atomicAdd(&q->tail, 1ull);
-            *reinterpret_cast<volatile unsigned long long *>(slots + (t & mask)) = ((t + 1) << 32) | chain;
+            st_release_u64(slots + (t & mask), ((t + 1) << 32) | chain);
         }
     }
+    __syncwarp();
 }
 
-__device__ __forceinline__ void load_state(const uint32_t *__restrict__ state, uint64_t G, uint64_t g,
-                                           uint32_t (&r)[NBITS], uint32_t (&s)[NBITS])
+// State moves between SMs through L2: ld.cg / st.cg, addresses by pointer
+// bumping.  The kernels receive the state / accumulator base twice (an input
+// and an output parameter holding the same address): otherwise ptxas keeps the
+// 200 load addresses alive across the clock loop to reuse them for the
+// stores, and spills every one of them.  The accumulator store doubles as the
+// lane's release fence for everything it wrote in this job.
+__device__ __forceinline__ void bump(const uint32_t *&p, uint64_t stride)
 {
-#pragma unroll
-    for (int i = 0; i < NBITS; ++i) {
-        r[i] = __ldcg(state + (uint64_t)i * G + g);
-        s[i] = __ldcg(state + (uint64_t)(NBITS + i) * G + g);
-    }
+    p += stride;
+    asm volatile("" : "+l"(p));
 }
-__device__ __forceinline__ void store_state(uint32_t *__restrict__ state, uint64_t G, uint64_t g,
-                                            const uint32_t (&r)[NBITS], const uint32_t (&s)[NBITS])
+__device__ __forceinline__ void load_state(const uint32_t *__restrict__ state, const unsigned long long *acc,
+                                           uint64_t G, uint64_t g, uint32_t (&r)[NBITS], uint32_t (&s)[NBITS],
+                                           unsigned long long &a)
 {
+    const uint32_t *p = state + g;
 #pragma unroll
     for (int i = 0; i < NBITS; ++i) {
-        __stcg(state + (uint64_t)i * G + g, r[i]);
-        __stcg(state + (uint64_t)(NBITS + i) * G + g, s[i]);
+        r[i] = __ldcg(p);
+        bump(p, G);
     }
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        s[i] = __ldcg(p);
+        bump(p, G);
+    }
+    a = __ldcg(acc + g);
+}
+__device__ __forceinline__ void store_state(uint32_t *__restrict__ state, unsigned long long *acc, uint64_t G,
+                                            uint64_t g, const uint32_t (&r)[NBITS], const uint32_t (&s)[NBITS],
+                                            unsigned long long a)
+{
+    const uint32_t *p = state + g;
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        __stcg(const_cast<uint32_t *>(p), r[i]);
+        bump(p, G);
+    }
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        __stcg(const_cast<uint32_t *>(p), s[i]);
+        bump(p, G);
+    }
+    st_release_u64(acc + g, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -350,21 +439,24 @@ __device__ __forceinline__ void store_state(uint32_t *__restrict__ state, uint64
 // accumulator live in HBM between chunks and between calls.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(BLOCK, 1)
-gen_colmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc,
-                    uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T, uint32_t chunk,
+gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
+                    unsigned long long *acc_out, uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T, uint32_t chunk,
                     uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots, uint32_t mask,
-                    uint32_t *progress)
+                    uint32_t *progress, Trace tr)
 {
     uint32_t chain;
-    while (sched_pop(q, slots, mask, chain)) {
+    for (;;) {
+        const unsigned long long t_pop = tr.rec ? gtime() : 0ull;
+        if (!sched_pop(q, slots, mask, chain)) break;
+        const unsigned long long t_start = tr.rec ? gtime() : 0ull;
         const uint32_t k = __ldcg(progress + chain);
         const uint64_t g = (uint64_t)chain * 32 + (threadIdx.x & 31u);
         const uint64_t t0 = (uint64_t)k * chunk;
         const uint64_t tc = T - t0 < chunk ? T - t0 : chunk;
         if (g < G) {
             uint32_t r[NBITS], s[NBITS];
-            load_state(state, G, g, r, s);
-            unsigned long long a = __ldcg(acc + g);
+            unsigned long long a;
+            load_state(state, acc, G, g, r, s, a);
             uint32_t *p = out + t0 * stride + g;
 #pragma unroll 1
             for (uint64_t t = 0; t < tc; ++t) {
@@ -374,10 +466,10 @@ gen_colmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict
                 acc_add(a, z);
                 clock<false, false>(r, s, 0u);
             }
-            store_state(state, G, g, r, s);
-            __stcg(acc + g, a);
+            store_state(state_out, acc_out, G, g, r, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
+        trace_job(tr, chain, k, t_pop, t_start);
     }
 }
 
@@ -418,7 +510,8 @@ __device__ __forceinline__ void bytes4x4(const uint32_t (&x)[4], uint32_t (&y)[4
 
 template <bool ALIGNED16>
 __global__ void __launch_bounds__(BLOCK, 1)
-gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc, uint8_t *__restrict__ out,
+gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
+                    unsigned long long *acc_out, uint8_t *__restrict__ out,
                     uint64_t pitch, uint64_t N, uint64_t G, uint64_t T, uint32_t chunk, uint32_t chunks_per_chain,
                     SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress)
 {
@@ -432,8 +525,8 @@ gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict
         const uint64_t tc = T - c0 < chunk ? T - c0 : chunk;
         if (g < G) {
             uint32_t r[NBITS], s[NBITS];
-            load_state(state, G, g, r, s);
-            unsigned long long a = __ldcg(acc + g);
+            unsigned long long a;
+            load_state(state, acc, G, g, r, s, a);
             uint8_t *rows = out + 32 * g * pitch + (c0 >> 3);
             const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;  // rows of this group that exist
 
@@ -493,8 +586,7 @@ gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict
                         }
                 }
             }
-            store_state(state, G, g, r, s);
-            __stcg(acc + g, a);
+            store_state(state_out, acc_out, G, g, r, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }

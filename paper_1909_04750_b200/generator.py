@@ -88,9 +88,33 @@ class MickeyGenerator:
     def set_async(self, flag: bool):
         self._ck(self._lib.mk2_set_async(self._ctx, int(bool(flag))), "mk2_set_async")
 
+    def last_plan(self):
+        """(threads per CTA, clocks per chunk) of the most recent keystream launch."""
+        b, c = C.c_int(), C.c_uint32()
+        self._ck(self._lib.mk2_last_plan(self._ctx, C.byref(b), C.byref(c)), "mk2_last_plan")
+        return b.value, c.value
+
     def set_block_threads(self, threads: int):
         """Tuning knob: threads per CTA of the clocking kernels (32..256)."""
         self._ck(self._lib.mk2_set_block_threads(self._ctx, int(threads)), "mk2_set_block_threads")
+
+    TRACE_DTYPE = np.dtype([("chain", "<u4"), ("k", "<u4"), ("smid", "<u4"), ("warp", "<u4"),
+                            ("t_pop", "<u8"), ("t_start", "<u8"), ("t_end", "<u8"), ("pad", "<u8")])
+
+    def set_trace(self, capacity: int):
+        """Diagnostics: record (chain, chunk, SM, warp, timestamps) per scheduled job."""
+        self._ck(self._lib.mk2_set_trace(self._ctx, int(capacity)), "mk2_set_trace")
+        self._trace_cap = int(capacity)
+
+    def read_trace(self) -> np.ndarray:
+        cap = getattr(self, "_trace_cap", 0)
+        rec = np.zeros(cap, self.TRACE_DTYPE)
+        n = C.c_uint64()
+        self._ck(self._lib.mk2_read_trace(self._ctx, _ptr(rec), cap, C.byref(n)), "mk2_read_trace")
+        return rec[: n.value]
+
+    def set_max_ctas(self, ctas: int):
+        self._ck(self._lib.mk2_set_max_ctas(self._ctx, int(ctas)), "mk2_set_max_ctas")
 
     def synchronize(self):
         self._ck(self._lib.mk2_sync(self._ctx), "mk2_sync")

@@ -19,11 +19,11 @@ sms = torch.cuda.get_device_properties(0).multi_processor_count
 print(json.dumps({"lop3_peak_Tlaneops": peak / 1e12, "probe_ms": ms, "sms": sms,
                   "implied_lanes_per_clk_per_sm_at_1965MHz": peak / sms / 1.965e9}))
 configs = []
-for block, chunk in ((256, 1 << 30), (256, 8192), (256, 4096), (256, 2048), (256, 1024), (128, 4096), (128, 1024)):
+for block, chunk in ((0, 0), (256, 1 << 30), (128, 4096), (256, 4096)):
     configs.append((block, chunk, sms * 8 * 32, "8 warps/SM exactly"))
     configs.append((block, chunk, 32768, "C2 geometry (2^20 instances)"))
-    if chunk in (1 << 30, 4096):
-        configs.append((block, chunk, 1 << 19, "C3 geometry (2^24 instances)"))
+    configs.append((block, chunk, 1 << 19, "C3 geometry (2^24 instances)"))
+    configs.append((block, chunk, 50000, "odd: 1.6M instances"))
 for layout in ("col", "row"):
     for block, chunk, G, label in configs:
         n = G * 32
@@ -42,7 +42,7 @@ for layout in ("col", "row"):
             fn()
             best = min(best, gen.last_kernel_ms)
         ops = n * T * 327 / 32
-        print(json.dumps({"layout": layout, "block": block, "chunk": chunk, "G": G, "label": label, "T": T, "ms": round(best, 3),
+        print(json.dumps({"layout": layout, "block": block, "chunk": chunk, "plan": gen.last_plan(), "G": G, "label": label, "T": T, "ms": round(best, 3),
                           "Tbps": round(n * T / best / 1e9, 4), "lop3_frac": round(ops / (best * 1e-3) / peak, 4)}))
         del out
 gen.close()
