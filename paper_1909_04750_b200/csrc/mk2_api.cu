@@ -220,7 +220,9 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, uint32_t granule)
             const uint64_t keff = (T + c - 1) / c;
             const uint64_t jobs = chains * keff;
             const double rounds = (double)((jobs + workers - 1) / workers);
-            const double cost = rounds * c;  // time ~ rounds x chunk length
+            // time ~ rounds x (chunk length + hand-off); a hand-off costs about 30 clocks' worth
+            // (~10 us, exposed because a lone warp has no partner to overlap it with)
+            const double cost = rounds * ((double)c + 30.0);
             if (cost < best * 0.998) {
                 best = cost;
                 best_k = k;

@@ -180,24 +180,31 @@ init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_
 #pragma unroll
     for (int i = 0; i < NBITS; ++i) r[i] = s[i] = 0u;
 
+    // input words are fetched one clock ahead so the load latency hides behind a clock's LOP3s
     const uint32_t *p = mat + g;
     int c = 0;
+    uint32_t in_next = load_clocks > 0 ? __ldg(p) : 0u;
     if constexpr (RAGGED) {
         const uint32_t *pa = mat + (uint64_t)(lmax + KEY_BITS) * G + g;
+        uint32_t act_next = lmax > 0 ? __ldg(pa) : 0u;
 #pragma unroll 1
         for (; c < lmax; ++c) {
-            clock<true, true>(r, s, *p);
-            const uint32_t act = *pa;
-#pragma unroll
-            for (int i = 0; i < NBITS; ++i) { r[i] &= act; s[i] &= act; }
+            const uint32_t in = in_next, act = act_next;
             p += G;
             pa += G;
+            if (c + 1 < load_clocks) in_next = __ldg(p);
+            if (c + 1 < lmax) act_next = __ldg(pa);
+            clock<true, true>(r, s, in);
+#pragma unroll
+            for (int i = 0; i < NBITS; ++i) { r[i] &= act; s[i] &= act; }
         }
     }
 #pragma unroll 1
     for (; c < load_clocks; ++c) {
-        clock<true, true>(r, s, *p);
+        const uint32_t in = in_next;
         p += G;
+        if (c + 1 < load_clocks) in_next = __ldg(p);
+        clock<true, true>(r, s, in);
     }
 #pragma unroll 1
     for (int k = 0; k < PRECLOCKS; ++k) clock<true, false>(r, s, 0u);
@@ -569,8 +576,11 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                         }
 #pragma unroll
                         for (int qq = 0; qq < 4; ++qq)
-                            __stcs(reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch),
-                                   make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]));
+                            // default (write-back) policy on purpose: the other half of this 32-byte
+                            // sector arrives one drain later and must still find it in L2, otherwise the
+                            // partial sector costs a DRAM read-modify-write
+                            *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch) =
+                                make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]);
                     }
                 } else {
                     // ragged edge: short tail, partial last group or unaligned rows

@@ -11,8 +11,8 @@ import paper_1909_04750_b200 as pkg
 layout = sys.argv[1] if len(sys.argv) > 1 else "col"
 lg = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 T = int(sys.argv[3]) if len(sys.argv) > 3 else 8192
-block = int(sys.argv[4]) if len(sys.argv) > 4 else 256
-chunk = int(sys.argv[5]) if len(sys.argv) > 5 else 4096
+block = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+chunk = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 n = 1 << lg
 gen = pkg.MickeyGenerator(0)
 gen.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -28,4 +28,4 @@ else:
     for _ in range(2):
         gen.generate_rowmajor(T, out)
 torch.cuda.synchronize()
-print(layout, n, T, block, chunk, "ms", gen.last_kernel_ms, "Tb/s", n * T / gen.last_kernel_ms / 1e9)
+print(layout, n, T, gen.last_plan(), "ms", gen.last_kernel_ms, "Tb/s", n * T / gen.last_kernel_ms / 1e9)
