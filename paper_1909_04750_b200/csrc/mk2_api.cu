@@ -23,6 +23,7 @@ struct mk2_ctx {
     int device = 0;
     int sm_count = 0;
     cudaStream_t own = nullptr, stream = nullptr, copy = nullptr;
+    cudaMemPool_t pool = nullptr;  // private stream-ordered pool for scratch (kept warm: no trim at sync points)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t gen_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
     bool copy_pending[2] = {false, false};
@@ -150,7 +151,7 @@ int stage_input(mk2_ctx *ctx, const void *src, size_t bytes, const uint8_t **dev
         *dev = static_cast<const uint8_t *>(src);
         return MK2_OK;
     }
-    CK(cudaMallocAsync(owned, bytes, ctx->stream));
+    CK(cudaMallocFromPoolAsync(owned, bytes, ctx->pool, ctx->stream));
     CK(cudaMemcpyAsync(*owned, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
     *dev = static_cast<const uint8_t *>(*owned);
     return MK2_OK;
@@ -194,9 +195,8 @@ struct Plan {
     unsigned grid;
 };
 
-Plan make_plan(const mk2_ctx *ctx, uint64_t T, uint32_t granule)
+Plan make_plan(const mk2_ctx *ctx, uint64_t T, uint32_t granule, uint64_t chains)
 {
-    const uint64_t chains = (ctx->G + 31) / 32;
     const uint64_t sms = (uint64_t)ctx->sm_count;
     Plan p{};
     auto round_chunk = [&](uint64_t c) {
@@ -238,9 +238,8 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, uint32_t granule)
 }
 
 // Scheduler reset for one launch.
-int launch_sched(mk2_ctx *ctx, const Plan &p)
+int launch_sched(mk2_ctx *ctx, const Plan &p, uint64_t chains)
 {
-    const uint64_t chains = (ctx->G + 31) / 32;
     if ((uint64_t)p.cpc * chains >= 0xFFFFFFFFull) return fail(ctx, MK2_E_ARG, "too many chunks: raise mk2_set_chunk_clocks");
     sched_init_kernel<<<(ctx->ring + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_queue, ctx->d_slots, ctx->d_progress,
                                                                         (uint32_t)chains, p.cpc, ctx->ring);
@@ -253,8 +252,9 @@ int launch_sched(mk2_ctx *ctx, const Plan &p)
 
 int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 {
-    const Plan p = make_plan(ctx, T, 1);
-    int rc = launch_sched(ctx, p);
+    const uint64_t chains = (ctx->G + 31) / 32;
+    const Plan p = make_plan(ctx, T, 1, chains);
+    int rc = launch_sched(ctx, p, chains);
     if (rc) return rc;
     gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out,
                                                              stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
@@ -264,20 +264,22 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
     return MK2_OK;
 }
 
-int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch)
+// Row-major keystream of chains [chain_base, chain_base + nchains); `out` = row of the first
+// instance of chain_base.
+int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t chain_base, uint64_t nchains)
 {
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
-    const Plan p = make_plan(ctx, T, 8 * ROW_GROUPS);  // whole 128-clock tiles
-    int rc = launch_sched(ctx, p);
+    const Plan p = make_plan(ctx, T, 8 * ROW_GROUPS, nchains);  // whole 128-clock tiles
+    int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
     if (aligned)
         gen_rowmajor_kernel<true><<<p.grid, p.block, ROW_SMEM_BYTES, ctx->stream>>>(
             ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
-            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress);
+            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
     else
         gen_rowmajor_kernel<false><<<p.grid, p.block, ROW_SMEM_BYTES, ctx->stream>>>(
             ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
-            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress);
+            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -353,6 +355,20 @@ int mk2_create(int device, mk2_ctx **out)
         e = cudaEventCreateWithFlags(&c->gen_done[b], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_done[b], cudaEventDisableTiming);
     }
+    if (e == cudaSuccess) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        e = cudaMemPoolCreate(&c->pool, &props);
+        if (e == cudaSuccess) {
+            // scratch freed with cudaFreeAsync stays in the pool instead of being unmapped at the next
+            // synchronisation (the default pool's behaviour cost ~40 ms per 1.3 GB re-allocation)
+            unsigned long long keep = ~0ull;
+            e = cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_sum, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_queue, sizeof(SchedQueue));
     if (e == cudaSuccess)
@@ -390,6 +406,7 @@ int mk2_destroy(mk2_ctx *ctx)
     if (ctx->d_progress) cudaFree(ctx->d_progress);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     delete ctx;
@@ -552,7 +569,7 @@ int mk2_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs
     if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
     if ((rc = stage_input(ctx, iv_bits ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
     const int load = (int)iv_bits + KEY_BITS;
-    CK(cudaMallocAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->stream));
+    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->pool, ctx->stream));
     pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, N, ctx->G, mat);
     CK(cudaGetLastError());
     ctx->last_launches++;
@@ -593,7 +610,7 @@ int mk2_init_ragged(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint3
     if ((rc = stage_input(ctx, lmax ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
     if ((rc = stage_input(ctx, iv_nbits, N, &dn, &on))) return rc;
     const int load = lmax + KEY_BITS;
-    CK(cudaMallocAsync(&mat, sizeof(uint32_t) * (size_t)(2 * lmax + KEY_BITS + 1) * ctx->G, ctx->stream));
+    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)(2 * lmax + KEY_BITS + 1) * ctx->G, ctx->pool, ctx->stream));
     pack_ragged_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, dn, lmax, N, ctx->G, mat);
     CK(cudaGetLastError());
     ctx->last_launches++;
@@ -616,7 +633,7 @@ int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_inde
     for (int i = 2; i < 10; ++i) lo = (lo << 8) | key[i];
     if ((rc = begin_timing(ctx))) return rc;
     uint32_t *mat = nullptr;
-    CK(cudaMallocAsync(&mat, sizeof(uint32_t) * (size_t)160 * ctx->G, ctx->stream));
+    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)160 * ctx->G, ctx->pool, ctx->stream));
     pack_counter_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(hi, lo, first_index, ctx->G, mat);
     CK(cudaGetLastError());
     ctx->last_launches++;
@@ -653,8 +670,11 @@ int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_w
             CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
             CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
             uint8_t *dst = static_cast<uint8_t *>(out) + t0 * stride_words * sizeof(uint32_t);
-            CK(cudaMemcpy2DAsync(dst, stride_words * sizeof(uint32_t), ctx->d_stage[b], row_bytes, row_bytes, tc,
-                                 cudaMemcpyDeviceToHost, ctx->copy));
+            if (stride_words == ctx->G)
+                CK(cudaMemcpyAsync(dst, ctx->d_stage[b], row_bytes * tc, cudaMemcpyDeviceToHost, ctx->copy));
+            else
+                CK(cudaMemcpy2DAsync(dst, stride_words * sizeof(uint32_t), ctx->d_stage[b], row_bytes, row_bytes, tc,
+                                     cudaMemcpyDeviceToHost, ctx->copy));
             CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
             ctx->copy_pending[b] = true;
         }
@@ -677,27 +697,41 @@ int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_by
     if (!out) return fail(ctx, MK2_E_ARG, "out is NULL");
     if (pitch_bytes < T / 8) return fail(ctx, MK2_E_ARG, "pitch_bytes smaller than T/8");
     if ((rc = begin_timing(ctx))) return rc;
+    const uint64_t chains = (ctx->G + 31) / 32;
     if (is_device_ptr(out)) {
-        if ((rc = launch_row(ctx, T, static_cast<uint8_t *>(out), pitch_bytes))) return rc;
+        if ((rc = launch_row(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, 0, chains))) return rc;
     } else {
-        // stage [N][tc/8] tiles; tc a multiple of 128 clocks keeps the 16-byte store path
-        const uint64_t min_bytes = ctx->N * 16;
-        const size_t want = std::max<size_t>(std::min<size_t>(STAGE_BYTES, ctx->N * ((T + 127) / 128 * 16)), min_bytes);
-        if ((rc = ensure_stage(ctx, want))) return rc;
-        const uint64_t chunk = std::max<uint64_t>(128, ctx->stage_bytes / ctx->N / 16 * 128);
+        // Host output: 2-D tiles [block of chains] x [time chunk] through two device staging
+        // buffers.  A tile is a contiguous run of instance rows, each >= 512 B wide whenever T
+        // allows, so the D2H copy is one wide 2-D (or plain 1-D) transfer; a chain block is
+        // large enough to occupy every worker warp.  Chains stay strictly serial in time
+        // because the time loop is the inner one.
+        const uint64_t block_chains = std::min<uint64_t>(chains, 2ull * 8ull * (uint64_t)ctx->sm_count);
+        const uint64_t block_rows = block_chains * 1024;
+        uint64_t tc_max = std::max<uint64_t>(128, (size_t(1) << 30) / block_rows / 16 * 128);  // <= 1 GiB per tile
+        tc_max = std::min<uint64_t>(tc_max, (T + 127) / 128 * 128);
+        if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
         int b = 0;
-        for (uint64_t t0 = 0; t0 < T; t0 += chunk, b ^= 1) {
-            const uint64_t tc = std::min(chunk, T - t0);
-            const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
-            if ((rc = acquire_stage(ctx, b))) return rc;
-            if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp))) return rc;
-            CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
-            CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
-            uint8_t *dst = static_cast<uint8_t *>(out) + t0 / 8;
-            CK(cudaMemcpy2DAsync(dst, pitch_bytes, ctx->d_stage[b], sp, tc / 8, ctx->N, cudaMemcpyDeviceToHost,
-                                 ctx->copy));
-            CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
-            ctx->copy_pending[b] = true;
+        for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {
+            const uint64_t nch = std::min(block_chains, chains - c0);
+            const uint64_t row0 = c0 * 1024;
+            const uint64_t nrows = std::min<uint64_t>(nch * 1024, ctx->N - row0);
+            for (uint64_t t0 = 0; t0 < T; t0 += tc_max, b ^= 1) {
+                const uint64_t tc = std::min(tc_max, T - t0);
+                const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
+                if ((rc = acquire_stage(ctx, b))) return rc;
+                if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp, c0, nch))) return rc;
+                CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
+                CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
+                uint8_t *dst = static_cast<uint8_t *>(out) + row0 * pitch_bytes + t0 / 8;
+                if (sp == tc / 8 && pitch_bytes == sp)
+                    CK(cudaMemcpyAsync(dst, ctx->d_stage[b], nrows * sp, cudaMemcpyDeviceToHost, ctx->copy));
+                else
+                    CK(cudaMemcpy2DAsync(dst, pitch_bytes, ctx->d_stage[b], sp, tc / 8, nrows, cudaMemcpyDeviceToHost,
+                                         ctx->copy));
+                CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
+                ctx->copy_pending[b] = true;
+            }
         }
         if ((rc = drain_copies(ctx))) return rc;
     }

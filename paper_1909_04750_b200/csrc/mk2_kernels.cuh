@@ -304,14 +304,14 @@ __device__ __forceinline__ uint32_t smid()
     return v;
 }
 __device__ __forceinline__ void trace_job(const Trace &tr, uint32_t chain, uint32_t k, unsigned long long t_pop,
-                                          unsigned long long t_start)
+                                          unsigned long long t_start, unsigned long long t_end)
 {
     if (tr.rec && (threadIdx.x & 31u) == 0) {
         const unsigned long long i = atomicAdd(tr.count, 1ull);
         if (i < tr.capacity) {
             TraceRec r;
             r.chain = chain; r.k = k; r.smid = smid(); r.warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-            r.t_pop = t_pop; r.t_start = t_start; r.t_end = gtime(); r.pad = 0;
+            r.t_pop = t_pop; r.t_start = t_start; r.t_end = t_end; r.pad = 0;
             tr.rec[i] = r;
         }
     }
@@ -475,8 +475,9 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             }
             store_state(state_out, acc_out, G, g, r, s, a);
         }
+        const unsigned long long t_end = tr.rec ? gtime() : 0ull;  // before the chain is handed on
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
-        trace_job(tr, chain, k, t_pop, t_start);
+        trace_job(tr, chain, k, t_pop, t_start, t_end);
     }
 }
 
@@ -520,21 +521,22 @@ __global__ void __launch_bounds__(BLOCK, 1)
 gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
                     unsigned long long *acc_out, uint8_t *__restrict__ out,
                     uint64_t pitch, uint64_t N, uint64_t G, uint64_t T, uint32_t chunk, uint32_t chunks_per_chain,
-                    SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress)
+                    SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress, uint32_t chain_base)
 {
     extern __shared__ uint32_t tile[];  // [8 * ROW_GROUPS clocks][BLOCK]
     uint32_t *col = tile + threadIdx.x;
     uint32_t chain;
     while (sched_pop(q, slots, mask, chain)) {
+        // chains [chain_base, chain_base + n) are scheduled; `out` row 0 is the first instance of chain_base
         const uint32_t k = __ldcg(progress + chain);
-        const uint64_t g = (uint64_t)chain * 32 + (threadIdx.x & 31u);
+        const uint64_t g = (uint64_t)(chain_base + chain) * 32 + (threadIdx.x & 31u);
         const uint64_t c0 = (uint64_t)k * chunk;  // chunk is a multiple of 128 clocks
         const uint64_t tc = T - c0 < chunk ? T - c0 : chunk;
         if (g < G) {
             uint32_t r[NBITS], s[NBITS];
             unsigned long long a;
             load_state(state, acc, G, g, r, s, a);
-            uint8_t *rows = out + 32 * g * pitch + (c0 >> 3);
+            uint8_t *rows = out + 32 * (g - (uint64_t)chain_base * 32) * pitch + (c0 >> 3);
             const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;  // rows of this group that exist
 
 #pragma unroll 1

@@ -369,6 +369,26 @@ def test_c2_instance_count_sampled_and_checksummed(pkg, golden, oracle, torch_cu
         gen.set_stream(None)
 
 
+def test_rowmajor_host_output_tiles(pkg, oracle):
+    """Host row-major output crosses several [chain block] x [time chunk] staging tiles."""
+    N, T = 32 * 32 * 2400 + 40, 4096 + 256          # > 2 x 8 x 148 chains -> two chain blocks
+    key = bytes.fromhex("0123456789abcdef0123")
+    with pkg.MickeyGenerator(0) as gen:
+        gen.init_counter(key, 0, N)
+        rows = np.zeros((N, T // 8 + 5), np.uint8)   # pitch wider than the row
+        gen.generate_rowmajor(T, rows, pitch_bytes=rows.shape[1])
+        csum = gen.checksum()
+        gen.init_counter(key, 0, N)
+        gen.generate_colmajor(T)
+        assert gen.checksum() == csum
+    assert not rows[:, T // 8:].any()
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([[0, 1023, 1024, 2368 * 1024 - 1, 2368 * 1024, N - 1], rng.integers(0, N, 60)]))
+    for n in idx:
+        keys, ivs = oracle.counter_material(key, int(n), 1)
+        assert rows[n, : T // 8].tobytes() == oracle.bulk_rowmajor(keys, ivs, 80, T)[0].tobytes(), n
+
+
 def test_c5_init_dominated_explicit_material(pkg, oracle, torch_cuda):
     """BASELINE config 5 shape (fresh key/IV pairs x 1 Kbit) at 2^20 pairs: explicit random
     material from host arrays, row-major output to the host, sampled rows vs the oracle."""
@@ -379,3 +399,66 @@ def test_c5_init_dominated_explicit_material(pkg, oracle, torch_cuda):
     idx = np.unique(np.concatenate([[0, 1, 31, 32, N - 1], rng.integers(0, N, 200)]))
     want = oracle.bulk_rowmajor(keys[idx], ivs[idx], 80, T)
     assert np.array_equal(rows[idx], want)
+
+
+# ---------------------------------------------------------------- persistent scheduler
+
+@pytest.mark.parametrize("block,chunk", [(0, 0), (32, 128), (64, 384), (128, 1000), (256, 128), (256, 1 << 30)])
+def test_schedule_knobs_do_not_change_bits(pkg, oracle, block, chunk):
+    """Any worker-warp count / chunk length must give the same keystream (column- and row-major),
+    including a partial last chain (G % 32 != 0), a partial last group (N % 32 != 0) and chunk tails."""
+    N, T = 32 * 75 + 9, 1160
+    keys, ivs = random_arrays(31337, N)
+    want_c = oracle.bulk_colmajor(keys, ivs, 80, T)
+    want_r = oracle.bulk_rowmajor(keys, ivs, 80, T)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_block_threads(block)
+        gen.set_chunk_clocks(chunk)
+        got_c = gen.init_material(keys, ivs, 80).generate_colmajor(T)
+        plan = gen.last_plan()
+        assert plan[0] in (32, 64, 128, 256) and plan[1] >= 1
+        c1 = gen.checksum()
+        got_r = gen.init_material(keys, ivs, 80).generate_rowmajor(T)
+        assert gen.checksum() == c1
+    assert np.array_equal(got_c, want_c)
+    assert np.array_equal(got_r, want_r)
+
+
+def test_many_chains_many_chunks_and_trace(pkg, oracle, torch_cuda):
+    """More chains than worker warps, tiny chunks: every chain migrates between SMs many times."""
+    torch = torch_cuda
+    N, T = 32 * 32 * 700, 640          # 700 chains
+    key = bytes.fromhex("00112233445566778899")
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_chunk_clocks(128)
+        gen.set_trace(1 << 14)
+        gen.init_counter(key, 64, N)
+        col = torch.empty((T, N // 32), dtype=torch.int32, device="cuda")
+        gen.generate_colmajor(T, col.data_ptr())
+        tr = gen.read_trace()
+        assert len(tr) == 700 * 5                       # one record per (chain, chunk)
+        assert set(zip(tr["chain"].tolist(), tr["k"].tolist())) == {(c, k) for c in range(700) for k in range(5)}
+        order = np.lexsort((tr["k"], tr["chain"]))
+        t = tr[order]
+        same = t["chain"][1:] == t["chain"][:-1]
+        assert np.all(t["t_start"][1:][same] >= t["t_end"][:-1][same])   # chunks of a chain never overlap
+        assert len(np.unique(tr["smid"])) > 100         # work really spread over the SMs
+        gen.set_trace(0)
+        gen.set_chunk_clocks(0)
+        gen.init_counter(key, 64, N)
+        col2 = torch.empty_like(col)
+        gen.generate_colmajor(T, col2.data_ptr())
+        assert torch.equal(col, col2)
+    for g in (0, 1023, 22398):
+        g &= ~1
+        keys, ivs = oracle.counter_material(key, 64 + 32 * g, 64)
+        assert np.array_equal(col[:, g:g + 2].cpu().numpy().view(np.uint32), oracle.bulk_colmajor(keys, ivs, 80, T))
+
+
+def test_knob_validation(pkg):
+    gen = pkg.MickeyGenerator(0)
+    with pytest.raises(ValueError):
+        gen.set_block_threads(48)
+    with pytest.raises(ValueError):
+        gen.set_chunk_clocks(64)
+    gen.close()
