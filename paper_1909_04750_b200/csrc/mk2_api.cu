@@ -189,22 +189,27 @@ int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bo
 // mk2_set_block_threads / mk2_set_chunk_clocks override the automatic choice.
 // ---------------------------------------------------------------------------
 struct Plan {
-    int block;        // threads per CTA (4 or 8 worker warps), one CTA per SM
+    int tg;           // row-major only: 8-clock groups per drain (16 or 32)
+    int block;        // threads per CTA (4, 6 or 8 worker warps), one CTA per SM
     uint32_t chunk;   // clocks per chunk
     uint32_t cpc;     // chunks per chain
     unsigned grid;
 };
 
-Plan make_plan(const mk2_ctx *ctx, uint64_t T, uint32_t granule, uint64_t chains)
+Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
 {
     const uint64_t sms = (uint64_t)ctx->sm_count;
     Plan p{};
+    // row-major: 7 warps per SM x 1 KiB per thread = 224 KiB of the 227 KiB shared memory leave room
+    // for 256-clock (full 32-byte sector) staging tiles
+    p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? (rowmajor ? 224 : 256) : 128);
+    p.tg = p.block <= 224 ? 32 : 16;  // strides: <= 128 -> 128, <= 192 -> 192, <= 224 -> 224, else (16, 256)
+    const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : 1u;
     auto round_chunk = [&](uint64_t c) {
         c = std::max<uint64_t>(c, granule);
         c = (c + granule - 1) / granule * granule;
-        return (uint32_t)std::min<uint64_t>(c, 0x7FFFFF80ull);
+        return (uint32_t)std::min<uint64_t>(c, 0x7FFFFF00ull);
     };
-    p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? 256 : 128);
     const uint64_t workers = sms * (uint64_t)(p.block / 32);
     if (ctx->chunk_user) {
         p.chunk = round_chunk(ctx->chunk_user);
@@ -253,7 +258,7 @@ int launch_sched(mk2_ctx *ctx, const Plan &p, uint64_t chains)
 int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 {
     const uint64_t chains = (ctx->G + 31) / 32;
-    const Plan p = make_plan(ctx, T, 1, chains);
+    const Plan p = make_plan(ctx, T, false, chains);
     int rc = launch_sched(ctx, p, chains);
     if (rc) return rc;
     gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out,
@@ -269,17 +274,22 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t chain_base, uint64_t nchains)
 {
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
-    const Plan p = make_plan(ctx, T, 8 * ROW_GROUPS, nchains);  // whole 128-clock tiles
+    const Plan p = make_plan(ctx, T, true, nchains);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
-    if (aligned)
-        gen_rowmajor_kernel<true><<<p.grid, p.block, ROW_SMEM_BYTES, ctx->stream>>>(
-            ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
-            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
-    else
-        gen_rowmajor_kernel<false><<<p.grid, p.block, ROW_SMEM_BYTES, ctx->stream>>>(
-            ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
-            ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+    // staging geometry: (TG, stride) = (32, 128) | (32, 192) | (16, 256); the stride is a template
+    // parameter so that every smem offset in the drain loops is an immediate
+    const int ts = p.tg == 32 ? (p.block <= 128 ? 128 : p.block <= 192 ? 192 : 224) : 256;
+    const size_t smem = (size_t)row_smem_bytes(p.tg, ts);
+#define MK2_ROW_LAUNCH(AL, TGV, TSV)                                                                         \
+    gen_rowmajor_kernel<AL, TGV, TSV><<<p.grid, p.block, smem, ctx->stream>>>(                              \
+        ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,  \
+        ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base)
+    if (ts == 128) { if (aligned) MK2_ROW_LAUNCH(true, 32, 128); else MK2_ROW_LAUNCH(false, 32, 128); }
+    else if (ts == 192) { if (aligned) MK2_ROW_LAUNCH(true, 32, 192); else MK2_ROW_LAUNCH(false, 32, 192); }
+    else if (ts == 224) { if (aligned) MK2_ROW_LAUNCH(true, 32, 224); else MK2_ROW_LAUNCH(false, 32, 224); }
+    else { if (aligned) MK2_ROW_LAUNCH(true, 16, 256); else MK2_ROW_LAUNCH(false, 16, 256); }
+#undef MK2_ROW_LAUNCH
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -371,10 +381,18 @@ int mk2_create(int device, mk2_ctx **out)
     }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_sum, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_queue, sizeof(SchedQueue));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM_BYTES);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(gen_rowmajor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM_BYTES);
+    const int row_smem_max = row_smem_bytes(32, 224);  // the largest staging tile: 224 KiB
+    auto opt_in = [&](auto kernel) {
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, row_smem_max);
+    };
+    opt_in(gen_rowmajor_kernel<true, 32, 128>);
+    opt_in(gen_rowmajor_kernel<false, 32, 128>);
+    opt_in(gen_rowmajor_kernel<true, 32, 192>);
+    opt_in(gen_rowmajor_kernel<false, 32, 192>);
+    opt_in(gen_rowmajor_kernel<true, 32, 224>);
+    opt_in(gen_rowmajor_kernel<false, 32, 224>);
+    opt_in(gen_rowmajor_kernel<true, 16, 256>);
+    opt_in(gen_rowmajor_kernel<false, 16, 256>);
     if (e != cudaSuccess) {
         std::string msg = std::string("context setup: ") + cudaGetErrorString(e);
         mk2_destroy(c);
@@ -708,8 +726,8 @@ int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_by
         // because the time loop is the inner one.
         const uint64_t block_chains = std::min<uint64_t>(chains, 2ull * 8ull * (uint64_t)ctx->sm_count);
         const uint64_t block_rows = block_chains * 1024;
-        uint64_t tc_max = std::max<uint64_t>(128, (size_t(1) << 30) / block_rows / 16 * 128);  // <= 1 GiB per tile
-        tc_max = std::min<uint64_t>(tc_max, (T + 127) / 128 * 128);
+        uint64_t tc_max = std::max<uint64_t>(256, (size_t(1) << 30) / block_rows / 32 * 256);  // <= 1 GiB per tile
+        tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
         if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
         int b = 0;
         for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {

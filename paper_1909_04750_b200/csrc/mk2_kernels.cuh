@@ -18,8 +18,11 @@
 namespace mk2 {
 
 constexpr int BLOCK = 256;           // 8 warps = 2 per SM sub-partition at 255 regs/thread
-constexpr int ROW_GROUPS = 16;       // 8-clock groups staged per drain = 16 bytes per instance row
-constexpr int ROW_SMEM_BYTES = 8 * ROW_GROUPS * BLOCK * 4;  // 128 KiB
+// Row-major staging: TG 8-clock groups per drain = TG bytes per instance row per drain.
+// TG = 32 (256 clocks, a full 32-byte sector per row) needs 1 KiB of shared memory per
+// thread, i.e. at most 6 worker warps per SM; TG = 16 allows 8 warps but writes half
+// sectors (measured: 4x the algorithmic DRAM traffic from read-modify-write).
+constexpr int row_smem_bytes(int tg, int threads) { return 8 * tg * threads * 4; }
 
 // ---------------------------------------------------------------------------
 // 8 x 32 bit-matrix transpose, in place: afterwards bit (8q + k) of w[b] is the
@@ -516,21 +519,22 @@ __device__ __forceinline__ void bytes4x4(const uint32_t (&x)[4], uint32_t (&y)[4
     y[3] = prmt(b01, b23, 0x7632);
 }
 
-template <bool ALIGNED16>
+template <bool ALIGNED16, int TG, int TS>
 __global__ void __launch_bounds__(BLOCK, 1)
 gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
                     unsigned long long *acc_out, uint8_t *__restrict__ out,
                     uint64_t pitch, uint64_t N, uint64_t G, uint64_t T, uint32_t chunk, uint32_t chunks_per_chain,
                     SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress, uint32_t chain_base)
 {
-    extern __shared__ uint32_t tile[];  // [8 * ROW_GROUPS clocks][BLOCK]
+    extern __shared__ uint32_t tile[];  // [8 * TG clocks][TS], TS >= blockDim.x
+    constexpr uint32_t ts = TS;         // tile stride: consecutive threads -> consecutive banks
     uint32_t *col = tile + threadIdx.x;
     uint32_t chain;
     while (sched_pop(q, slots, mask, chain)) {
         // chains [chain_base, chain_base + n) are scheduled; `out` row 0 is the first instance of chain_base
         const uint32_t k = __ldcg(progress + chain);
         const uint64_t g = (uint64_t)(chain_base + chain) * 32 + (threadIdx.x & 31u);
-        const uint64_t c0 = (uint64_t)k * chunk;  // chunk is a multiple of 128 clocks
+        const uint64_t c0 = (uint64_t)k * chunk;  // chunk is a multiple of 8 * TG clocks
         const uint64_t tc = T - c0 < chunk ? T - c0 : chunk;
         if (g < G) {
             uint32_t r[NBITS], s[NBITS];
@@ -540,49 +544,61 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;  // rows of this group that exist
 
 #pragma unroll 1
-            for (uint64_t t0 = 0; t0 < tc; t0 += 8 * ROW_GROUPS) {
-                const int nclk = (tc - t0) >= 8 * ROW_GROUPS ? 8 * ROW_GROUPS : (int)(tc - t0);
+            for (uint64_t t0 = 0; t0 < tc; t0 += 8 * TG) {
+                const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);
                 const int ngrp = nclk >> 3;
                 uint32_t *zp = col;
 #pragma unroll 1
                 for (int t = 0; t < nclk; ++t) {
                     const uint32_t z = keystream_word(r, s);
                     *zp = z;
-                    zp += BLOCK;
+                    zp += ts;
                     acc_add(a, z);
                     clock<false, false>(r, s, 0u);
                 }
-                // ---- pass 1: bit transposes, in place in the smem column
+                // ---- pass 1: bit transposes, in place in the smem column; the next group's 8 words
+                // are fetched while the current group is transposed (a lone warp has nobody else to
+                // hide the LDS latency behind)
+                {
+                    uint32_t nx[8];
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) nx[m] = col[m * ts];
 #pragma unroll 1
-                for (int grp = 0; grp < ngrp; ++grp) {
-                    uint32_t z[8];
-                    uint32_t *gp = col + grp * 8 * BLOCK;
+                    for (int grp = 0; grp < ngrp; ++grp) {
+                        uint32_t z[8];
+                        uint32_t *gp = col + grp * 8 * ts;
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) z[7 - m] = gp[m * BLOCK];  // clock m -> bit 7 - m (MSB-first)
-                    transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
+                        for (int m = 0; m < 8; ++m) z[7 - m] = nx[m];  // clock m -> bit 7 - m (MSB-first)
+                        if (grp + 1 < ngrp) {
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) gp[kk * BLOCK] = z[kk];
+                            for (int m = 0; m < 8; ++m) nx[m] = gp[(8 + m) * ts];
+                        }
+                        transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) gp[kk * ts] = z[kk];
+                    }
                 }
-                // ---- pass 2: 16 bytes (or the tail) per instance row
+                // ---- pass 2: TG bytes (or the tail) per instance row, 16 bytes per store; the two
+                // halves of a 32-byte sector are stored back to back so they merge in L2
                 uint8_t *dst = rows + (t0 >> 3);
-                if (ALIGNED16 && ngrp == ROW_GROUPS && nrows == 32) {
+                if (ALIGNED16 && ngrp == TG && nrows == 32) {
 #pragma unroll 1
                     for (int kk = 0; kk < 8; ++kk) {
-                        uint32_t y[4][4];  // [g4][q]
+#pragma unroll 1
+                        for (int half = 0; half < TG / 16; ++half) {
+                            uint32_t y[4][4];  // [g4][q]
 #pragma unroll
-                        for (int g4 = 0; g4 < 4; ++g4) {
-                            uint32_t x[4];
+                            for (int g4 = 0; g4 < 4; ++g4) {
+                                uint32_t x[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) x[u] = col[((4 * g4 + u) * 8 + kk) * BLOCK];
-                            bytes4x4(x, y[g4]);
+                                for (int u = 0; u < 4; ++u) x[u] = col[((16 * half + 4 * g4 + u) * 8 + kk) * ts];
+                                bytes4x4(x, y[g4]);
+                            }
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half) =
+                                    make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]);
                         }
-#pragma unroll
-                        for (int qq = 0; qq < 4; ++qq)
-                            // default (write-back) policy on purpose: the other half of this 32-byte
-                            // sector arrives one drain later and must still find it in L2, otherwise the
-                            // partial sector costs a DRAM read-modify-write
-                            *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch) =
-                                make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]);
                     }
                 } else {
                     // ragged edge: short tail, partial last group or unaligned rows
@@ -590,7 +606,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     for (int kk = 0; kk < 8; ++kk)
 #pragma unroll 1
                         for (int grp = 0; grp < ngrp; ++grp) {
-                            const uint32_t x = col[(grp * 8 + kk) * BLOCK];
+                            const uint32_t x = col[(grp * 8 + kk) * ts];
 #pragma unroll
                             for (int qq = 0; qq < 4; ++qq)
                                 if ((uint64_t)(8 * qq + kk) < nrows)
