@@ -94,6 +94,20 @@ int mk2_init_ragged(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint3
 int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_index, uint64_t N);
 
 /*
+ * Seed-derived material (pkg/src/slicerng/seedgen.py:57-86, derive_lane_material):
+ * AES-128 counter construction under a key derived from the 32-byte master
+ * seed; lane n gets key = stream[0:10], iv = stream[10:20].  The reference caps
+ * a seed at 64 lanes (seedgen.py:22); here first_lane + N may be up to 2^32
+ * (the lane field of the derivation block).  algo_tag: 1 aes-ctr, 2 grain,
+ * 3 mickey (seedgen.py:31).  mk2_derive_material writes keys/ivs (N x 10 bytes
+ * each, host or device); mk2_init_from_seed derives (tag 3) and initialises in
+ * one go without the material ever leaving the device.
+ */
+int mk2_derive_material(mk2_ctx *ctx, const uint8_t seed[32], uint32_t algo_tag, uint64_t first_lane, uint64_t N,
+                        uint8_t *keys, uint8_t *ivs);
+int mk2_init_from_seed(mk2_ctx *ctx, const uint8_t seed[32], uint64_t first_lane, uint64_t N);
+
+/*
  * T more keystream clocks, column-major ("bit-interleaved",
  * docs/conventions.md:61-63): out[t * stride_words + g] is a uint32 whose bit j
  * is keystream bit t of instance 32 g + j.  For N = 64 and stride 2 the buffer

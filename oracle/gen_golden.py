@@ -212,6 +212,25 @@ def main():
         "lane_major_2": ref_kernels.words_lane_major_bytes(w, 2).hex(),
     }
 
+    # --- seed derivation (seedgen.py:39-86) + the AES block vectors it rests on (vectors.py:78-93)
+    from slicerng import seedgen as ref_seedgen
+    from slicerng.aes_ctr import AesScalarTable
+
+    sg = []
+    for seed in (ref_bench.DEFAULT_SEED, bytes(range(32)), bytes([0xFF] * 31 + [0x01])):
+        master = ref_seedgen.MasterSeed(seed, "mickey", 64)
+        lanes = {}
+        for lane in (0, 1, 2, 31, 63):
+            m = ref_seedgen.derive_lane_material(master, lane)
+            lanes[str(lane)] = {"key": m.key.hex(), "iv": bytes(m.iv).hex()}
+        allm = ref_seedgen.derive_all(master)
+        blob = b"".join(m.key + bytes(m.iv) for m in allm)
+        sg.append({"seed": seed.hex(), "lanes": lanes, "all64_sha256": sha(blob)})
+    g["seedgen"] = sg
+    g["aes_blocks"] = [{"key": r.key.hex(), "pt": r.iv.hex(), "ct": r.ks.hex()} for r in ref_vectors.AES_BLOCK_VECTORS]
+    for r in ref_vectors.AES_BLOCK_VECTORS:
+        assert AesScalarTable(r.key).encrypt_block(r.iv) == r.ks
+
     OUT.parent.mkdir(parents=True, exist_ok=True)
     OUT.write_text(json.dumps(g, separators=(",", ":")))
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes)")

@@ -449,3 +449,112 @@ uint64_t mk2o_checksum_colmajor(const uint32_t *out, uint64_t T, uint64_t G, uin
         for (uint64_t g = 0; g < G; ++g) acc += (uint64_t)out[t * G + g] << (32 * ((g + g_offset) & 1));
     return acc;
 }
+
+/* ------------------------------------------------------------------------
+ * Seed derivation: pkg/src/slicerng/seedgen.py:57-86.
+ * AES-128 is the standard FIPS-197 cipher the reference implements as
+ * AesScalarTable (pkg/src/slicerng/aes_ctr.py:193-219); restated here with a
+ * computed S-box (GF(2^8) inverse + affine map) instead of a table literal.
+ *   dk      = AES_{seed[0:16]}(seed[16:32])                       seedgen.py:57-60
+ *   block_c = tag || lane (4 bytes BE) || c (4 bytes BE) || 0^7   seedgen.py:72-78
+ *   stream  = AES_dk(block_0) || AES_dk(block_1);  key = stream[0:10], iv = stream[10:20]
+ * tag: 1 = aes-ctr, 2 = grain, 3 = mickey (sorted names, seedgen.py:31).
+ * ---------------------------------------------------------------------- */
+static uint8_t AES_SBOX[256];
+static int aes_ready = 0;
+
+static uint8_t gf_mul(uint8_t a, uint8_t b)
+{
+    uint8_t p = 0;
+    for (int i = 0; i < 8; ++i) {
+        if (b & 1) p ^= a;
+        uint8_t hi = a & 0x80;
+        a = (uint8_t)(a << 1);
+        if (hi) a ^= 0x1B;
+        b >>= 1;
+    }
+    return p;
+}
+
+static void aes_build(void)
+{
+    if (aes_ready) return;
+    for (int x = 0; x < 256; ++x) {
+        uint8_t inv = 0;
+        if (x)
+            for (int y = 1; y < 256; ++y)
+                if (gf_mul((uint8_t)x, (uint8_t)y) == 1) { inv = (uint8_t)y; break; }
+        uint8_t r = inv, v = inv;
+        for (int k = 0; k < 4; ++k) { r = (uint8_t)((r << 1) | (r >> 7)); v ^= r; }
+        AES_SBOX[x] = v ^ 0x63;
+    }
+    aes_ready = 1;
+}
+
+static void aes_expand(const uint8_t key[16], uint8_t rk[11][16])
+{
+    memcpy(rk[0], key, 16);
+    uint8_t rcon = 1;
+    for (int r = 1; r <= 10; ++r) {
+        const uint8_t *p = rk[r - 1];
+        uint8_t t[4] = {AES_SBOX[p[13]], AES_SBOX[p[14]], AES_SBOX[p[15]], AES_SBOX[p[12]]};
+        t[0] ^= rcon;
+        rcon = gf_mul(rcon, 2);
+        for (int c = 0; c < 4; ++c)
+            for (int b = 0; b < 4; ++b) {
+                uint8_t prev = c ? rk[r][4 * (c - 1) + b] : t[b];
+                rk[r][4 * c + b] = p[4 * c + b] ^ prev;
+            }
+    }
+}
+
+static void aes_encrypt(const uint8_t rk[11][16], const uint8_t in[16], uint8_t out[16])
+{
+    uint8_t st[16], t[16];
+    for (int i = 0; i < 16; ++i) st[i] = in[i] ^ rk[0][i];
+    for (int r = 1; r <= 10; ++r) {
+        for (int i = 0; i < 16; ++i) t[i] = AES_SBOX[st[i]];
+        /* ShiftRows: byte i = row i%4, column i/4; row k rotates left by k */
+        for (int c = 0; c < 4; ++c)
+            for (int k = 0; k < 4; ++k) st[4 * c + k] = t[4 * ((c + k) & 3) + k];
+        if (r < 10)
+            for (int c = 0; c < 4; ++c) {
+                uint8_t *a = st + 4 * c, b0 = a[0], b1 = a[1], b2 = a[2], b3 = a[3], all = b0 ^ b1 ^ b2 ^ b3;
+                a[0] = b0 ^ all ^ gf_mul(b0 ^ b1, 2);
+                a[1] = b1 ^ all ^ gf_mul(b1 ^ b2, 2);
+                a[2] = b2 ^ all ^ gf_mul(b2 ^ b3, 2);
+                a[3] = b3 ^ all ^ gf_mul(b3 ^ b0, 2);
+            }
+        for (int i = 0; i < 16; ++i) st[i] ^= rk[r][i];
+    }
+    memcpy(out, st, 16);
+}
+
+void mk2o_aes128_encrypt(const uint8_t key[16], const uint8_t in[16], uint8_t out[16])
+{
+    uint8_t rk[11][16];
+    aes_build();
+    aes_expand(key, rk);
+    aes_encrypt(rk, in, out);
+}
+
+void mk2o_derive_material(const uint8_t seed[32], uint32_t tag, uint64_t first_lane, uint64_t n, uint8_t *keys,
+                          uint8_t *ivs)
+{
+    uint8_t rk[11][16], dk[16];
+    aes_build();
+    aes_expand(seed, rk);
+    aes_encrypt(rk, seed + 16, dk);
+    aes_expand(dk, rk);
+    for (uint64_t j = 0; j < n; ++j) {
+        uint64_t lane = first_lane + j;
+        uint8_t stream[32];
+        for (uint32_t c = 0; c < 2; ++c) {
+            uint8_t blk[16] = {(uint8_t)tag, (uint8_t)(lane >> 24), (uint8_t)(lane >> 16), (uint8_t)(lane >> 8),
+                               (uint8_t)lane, 0, 0, 0, (uint8_t)c, 0, 0, 0, 0, 0, 0, 0};
+            aes_encrypt(rk, blk, stream + 16 * c);
+        }
+        memcpy(keys + 10 * j, stream, 10);
+        memcpy(ivs + 10 * j, stream + 10, 10);
+    }
+}

@@ -60,6 +60,8 @@ def lib() -> C.CDLL:
         L.mk2o_checksum_colmajor.argtypes = [u32p, C.c_uint64, C.c_uint64, C.c_uint64]
         L.mk2o_checksum_colmajor.restype = C.c_uint64
         L.mk2o_max_threads.restype = C.c_int
+        L.mk2o_aes128_encrypt.argtypes = [u8p, u8p, u8p]
+        L.mk2o_derive_material.argtypes = [u8p, C.c_uint32, C.c_uint64, C.c_uint64, u8p, u8p]
         _lib = L
     return _lib
 
@@ -258,3 +260,25 @@ def timed_loops(nclocks: int, nworkers: int, ncalls: int = 1, states: np.ndarray
 
 def max_threads() -> int:
     return int(lib().mk2o_max_threads())
+
+
+ALGO_TAG_MICKEY = 3  # sorted(("aes-ctr", "grain", "mickey")).index("mickey") + 1, seedgen.py:31
+
+
+def aes128_encrypt(key: bytes, block: bytes) -> bytes:
+    k = np.frombuffer(bytes(key), np.uint8).copy()
+    b = np.frombuffer(bytes(block), np.uint8).copy()
+    out = np.zeros(16, np.uint8)
+    lib().mk2o_aes128_encrypt(_p(k, u8p), _p(b, u8p), _p(out, u8p))
+    return out.tobytes()
+
+
+def derive_material(seed: bytes, first_lane: int, n: int, tag: int = ALGO_TAG_MICKEY):
+    """Restates seedgen.derive_lane_material (seedgen.py:63-86) for lanes first_lane .. first_lane+n-1."""
+    if len(seed) != 32:
+        raise ValueError("master seed must be 32 bytes")
+    sd = np.frombuffer(bytes(seed), np.uint8).copy()
+    keys = np.zeros((n, 10), np.uint8)
+    ivs = np.zeros((n, 10), np.uint8)
+    lib().mk2o_derive_material(_p(sd, u8p), tag, first_lane, n, _p(keys, u8p), _p(ivs, u8p))
+    return keys, ivs

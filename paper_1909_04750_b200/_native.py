@@ -38,6 +38,8 @@ SYMBOLS = {
     "mk2_init_from_material": (C.c_int, [_vp, _u8p, _u8p, C.c_uint32, C.c_uint32, _u64]),
     "mk2_init_ragged": (C.c_int, [_vp, _u8p, _u8p, C.c_uint32, _u8p, _u64]),
     "mk2_init_counter_iv": (C.c_int, [_vp, _u8p, _u64, _u64]),
+    "mk2_derive_material": (C.c_int, [_vp, _u8p, C.c_uint32, _u64, _u64, _u8p, _u8p]),
+    "mk2_init_from_seed": (C.c_int, [_vp, _u8p, _u64, _u64]),
     "mk2_generate_colmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
     "mk2_generate_rowmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
     "mk2_clock": (C.c_int, [_vp, C.c_int, _u32p, _u64]),

@@ -11,6 +11,7 @@
 
 #include "../../include/mk2.h"
 #include "mk2_kernels.cuh"
+#include "mk2_seedgen.cuh"
 
 using namespace mk2;
 
@@ -657,6 +658,80 @@ int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_inde
     ctx->last_launches++;
     if ((rc = launch_init(ctx, mat, 160, 0, false))) return rc;
     CK(cudaFreeAsync(mat, ctx->stream));
+    return end_timing(ctx);
+}
+
+// Derive key/IV rows for lanes [first_lane, first_lane + N) into device buffers (stream ordered).
+static int derive_to_device(mk2_ctx *ctx, const uint8_t seed[32], uint32_t tag, uint64_t first_lane, uint64_t N,
+                            uint8_t *d_keys, uint8_t *d_ivs)
+{
+    if (!seed) return fail(ctx, MK2_E_ARG, "seed is NULL");
+    if (N == 0) return fail(ctx, MK2_E_ARG, "at least one lane is required");
+    if (first_lane + N > (1ull << 32) || first_lane + N < first_lane)
+        return fail(ctx, MK2_E_ARG, "lane index must fit the 32-bit field of the derivation block");
+    bool nonzero = false;
+    for (int i = 0; i < 32; ++i) nonzero |= seed[i] != 0;
+    if (!nonzero) return fail(ctx, MK2_E_ARG, "all-zero master seed rejected");
+    void *d_seed = nullptr, *d_rk = nullptr;
+    CK(cudaMallocFromPoolAsync(&d_seed, 32, ctx->pool, ctx->stream));
+    CK(cudaMallocFromPoolAsync(&d_rk, 44 * sizeof(uint32_t), ctx->pool, ctx->stream));
+    CK(cudaMemcpyAsync(d_seed, seed, 32, cudaMemcpyHostToDevice, ctx->stream));
+    seed_setup_kernel<<<1, 256, 0, ctx->stream>>>(static_cast<const uint8_t *>(d_seed), static_cast<uint32_t *>(d_rk));
+    CK(cudaGetLastError());
+    seed_derive_kernel<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(static_cast<const uint32_t *>(d_rk), tag,
+                                                                             first_lane, N, d_keys, d_ivs);
+    CK(cudaGetLastError());
+    ctx->last_launches += 2;
+    CK(cudaFreeAsync(d_seed, ctx->stream));
+    CK(cudaFreeAsync(d_rk, ctx->stream));
+    return MK2_OK;
+}
+
+int mk2_derive_material(mk2_ctx *ctx, const uint8_t seed[32], uint32_t algo_tag, uint64_t first_lane, uint64_t N,
+                        uint8_t *keys, uint8_t *ivs)
+{
+    if (!ctx) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (!keys || !ivs) return fail(ctx, MK2_E_ARG, "keys / ivs is NULL");
+    int rc = begin_timing(ctx);
+    if (rc) return rc;
+    const bool dk = is_device_ptr(keys), di = is_device_ptr(ivs);
+    void *tk = nullptr, *ti = nullptr;
+    if (!dk) CK(cudaMallocFromPoolAsync(&tk, N * 10, ctx->pool, ctx->stream));
+    if (!di) CK(cudaMallocFromPoolAsync(&ti, N * 10, ctx->pool, ctx->stream));
+    uint8_t *pk = dk ? keys : static_cast<uint8_t *>(tk), *pi = di ? ivs : static_cast<uint8_t *>(ti);
+    if ((rc = derive_to_device(ctx, seed, algo_tag, first_lane, N, pk, pi))) return rc;
+    if (!dk) CK(cudaMemcpyAsync(keys, tk, N * 10, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!di) CK(cudaMemcpyAsync(ivs, ti, N * 10, cudaMemcpyDeviceToHost, ctx->stream));
+    if (tk) CK(cudaFreeAsync(tk, ctx->stream));
+    if (ti) CK(cudaFreeAsync(ti, ctx->stream));
+    if ((rc = end_timing(ctx))) return rc;
+    if (!dk || !di) CK(cudaStreamSynchronize(ctx->stream));
+    return MK2_OK;
+}
+
+int mk2_init_from_seed(mk2_ctx *ctx, const uint8_t seed[32], uint64_t first_lane, uint64_t N)
+{
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
+    if ((rc = begin_timing(ctx))) return rc;
+    void *dk = nullptr, *di = nullptr;
+    uint32_t *mat = nullptr;
+    CK(cudaMallocFromPoolAsync(&dk, N * 10, ctx->pool, ctx->stream));
+    CK(cudaMallocFromPoolAsync(&di, N * 10, ctx->pool, ctx->stream));
+    if ((rc = derive_to_device(ctx, seed, 3u /* mickey */, first_lane, N, static_cast<uint8_t *>(dk),
+                               static_cast<uint8_t *>(di))))
+        return rc;
+    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)160 * ctx->G, ctx->pool, ctx->stream));
+    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(static_cast<const uint8_t *>(dk),
+                                                                       static_cast<const uint8_t *>(di), 10, 80, N,
+                                                                       ctx->G, mat);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    if ((rc = launch_init(ctx, mat, 160, 0, false))) return rc;
+    CK(cudaFreeAsync(mat, ctx->stream));
+    CK(cudaFreeAsync(dk, ctx->stream));
+    CK(cudaFreeAsync(di, ctx->stream));
     return end_timing(ctx);
 }
 

@@ -166,6 +166,24 @@ class MickeyGenerator:
                  "mk2_init_counter_iv")
         return self
 
+    def init_seed(self, seed: bytes, first_lane: int, n: int):
+        """Seed-derived key/IV material (seedgen.derive_lane_material) for lanes first_lane..+n-1, then init."""
+        sb = _seed_buf(seed)
+        self._ck(self._lib.mk2_init_from_seed(self._ctx, C.cast(sb, C.c_void_p), int(first_lane), int(n)),
+                 "mk2_init_from_seed")
+        return self
+
+    def derive_material(self, seed: bytes, first_lane: int, n: int, keys=None, ivs=None, algo_tag: int = 3):
+        """keys u8[n,10], ivs u8[n,10] derived on the GPU (numpy by default; torch/device buffers accepted)."""
+        sb = _seed_buf(seed)
+        if keys is None:
+            keys = np.empty((n, KEY_BYTES), np.uint8)
+        if ivs is None:
+            ivs = np.empty((n, 10), np.uint8)
+        self._ck(self._lib.mk2_derive_material(self._ctx, C.cast(sb, C.c_void_p), int(algo_tag), int(first_lane), int(n),
+                                               _ptr(keys), _ptr(ivs)), "mk2_derive_material")
+        return keys, ivs
+
     # -- generation -------------------------------------------------------
     def generate_colmajor(self, nclocks: int, out=None, stride_words: Optional[int] = None):
         """uint32 out[nclocks][G]; bit j of out[t][g] = keystream bit t of instance 32 g + j."""
@@ -227,6 +245,12 @@ class MickeyGenerator:
         v, ms = C.c_double(), C.c_float()
         self._ck(self._lib.mk2_lop3_peak(self._ctx, C.byref(v), C.byref(ms)), "mk2_lop3_peak")
         return v.value, ms.value
+
+
+def _seed_buf(seed: bytes):
+    if len(seed) != 32:
+        raise ValueError("master seed must be 32 bytes")
+    return (C.c_uint8 * 32).from_buffer_copy(bytes(seed))
 
 
 def _material_shape(keys, ivs, iv_bits):

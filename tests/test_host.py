@@ -137,3 +137,21 @@ def test_checksum_i64_roundtrip():
     for u in (0, 1, (1 << 63) - 1, 1 << 63, (1 << 64) - 1, 0xDB93F1AC2EF9D52E):
         assert sharding.from_i64(sharding.to_i64(u)) == u
     assert sharding.allreduce_checksum(0xDB93F1AC2EF9D52E) == 0xDB93F1AC2EF9D52E
+
+
+def test_master_seed_validation():
+    # seedgen.py:45-54
+    from paper_1909_04750_b200.seedgen import MasterSeed, SeedError
+
+    with pytest.raises(SeedError):
+        MasterSeed(bytes(31))
+    with pytest.raises(SeedError):
+        MasterSeed(bytes(32))
+    with pytest.raises(SeedError):
+        MasterSeed(bytes(range(32)), "rc4")
+    with pytest.raises(SeedError):
+        MasterSeed(bytes(range(32)), "grain")
+    with pytest.raises(SeedError):
+        MasterSeed(bytes(range(32)), "mickey", 0)
+    assert isinstance(SeedError("x"), ValueError)
+    assert MasterSeed(bytes(range(32)), "mickey", 1 << 20).lanes == 1 << 20

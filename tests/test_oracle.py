@@ -140,3 +140,24 @@ def test_bulk_ragged_and_partial_batches(oracle):
         assert row[n].tobytes() == ks
         lane = ((col[:, n // 32] >> np.uint32(n % 32)) & 1).astype(np.uint8)
         assert np.packbits(lane).tobytes() == ks
+
+
+def test_aes_blocks_and_seed_derivation(oracle, golden):
+    # vectors.py:78-93 (FIPS-197 examples) and seedgen.py:57-86 as run by the reference
+    for b in golden["aes_blocks"]:
+        assert oracle.aes128_encrypt(bytes.fromhex(b["key"]), bytes.fromhex(b["pt"])).hex() == b["ct"]
+    for rec in golden["seedgen"]:
+        keys, ivs = oracle.derive_material(bytes.fromhex(rec["seed"]), 0, 64)
+        for lane, m in rec["lanes"].items():
+            assert keys[int(lane)].tobytes().hex() == m["key"] and ivs[int(lane)].tobytes().hex() == m["iv"]
+        blob = b"".join(keys[j].tobytes() + ivs[j].tobytes() for j in range(64))
+        assert sha(blob) == rec["all64_sha256"]
+    # the bench-seed lanes of bench.py:43-45 are the same derivation
+    mats = golden["bench_seed"]["materials"]
+    keys, ivs = oracle.derive_material(bytes.fromhex(golden["seedgen"][0]["seed"]), 0, 64)
+    assert [keys[j].tobytes().hex() for j in range(64)] == [m["key"] for m in mats]
+    assert [ivs[j].tobytes().hex() for j in range(64)] == [m["iv"] for m in mats]
+    # windows agree with the whole
+    k2, i2 = oracle.derive_material(bytes.fromhex(golden["seedgen"][1]["seed"]), 40, 10)
+    kall, iall = oracle.derive_material(bytes.fromhex(golden["seedgen"][1]["seed"]), 0, 64)
+    assert np.array_equal(k2, kall[40:50]) and np.array_equal(i2, iall[40:50])
