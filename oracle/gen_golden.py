@@ -231,6 +231,31 @@ def main():
     for r in ref_vectors.AES_BLOCK_VECTORS:
         assert AesScalarTable(r.key).encrypt_block(r.iv) == r.ks
 
+    # --- CLI outputs (cli.py:102-152): `slicerng gen --algo mickey`, hex format
+    import tempfile
+    from slicerng import cli as ref_cli
+
+    cli_cases = []
+    for argv in (
+        ["--bits", "1024"],
+        ["--bits", "8192", "--lanes", "4", "--seed", "ab" * 32],
+        ["--bits", str(64 * 256), "--lanes", "64", "--seed", ref_bench.DEFAULT_SEED.hex()],
+        ["--bits", "128", "--key", "123456789abcdef01234", "--iv", "21436587"],
+        ["--bits", "1536", "--key", "123456789abcdef01234", "--lanes", "3"],
+        ["--bits", "2048", "--lanes", "7", "--interleave", "bit", "--seed", "cd" * 32],
+        ["--bits", "4096", "--lanes", "64", "--interleave", "bit"],
+        ["--bits", "1000", "--lanes", "5", "--interleave", "bit", "--key", "00112233445566778899", "--iv", "0102"],
+    ):
+        with tempfile.NamedTemporaryFile("r", suffix=".hex") as fh:
+            assert ref_cli.main(["gen", "--algo", "mickey", "--impl", "sliced", "--out", fh.name, *argv]) == 0
+            out = fh.read()
+        if "--interleave" not in argv:   # naive == sliced (cli.py:9-11)
+            with tempfile.NamedTemporaryFile("r", suffix=".hex") as fh2:
+                ref_cli.main(["gen", "--algo", "mickey", "--impl", "naive", "--out", fh2.name, *argv])
+                assert fh2.read() == out
+        cli_cases.append({"argv": argv, "hex": out})
+    g["cli_gen"] = cli_cases
+
     OUT.parent.mkdir(parents=True, exist_ok=True)
     OUT.write_text(json.dumps(g, separators=(",", ":")))
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes)")

@@ -504,3 +504,44 @@ def test_seed_derivation_matches_reference_and_oracle(pkg, golden, oracle, torch
         bs = golden["bench_seed"]
         row = gen.init_seed(bytes.fromhex(golden["seedgen"][0]["seed"]), 0, 64).generate_rowmajor(bs["nclocks"])
         assert sha(row.tobytes()) == bs["lane_major_sha256"]
+
+
+# ---------------------------------------------------------------- CLI
+
+def test_cli_gen_matches_reference_cli(pkg, golden, tmp_path):
+    from paper_1909_04750_b200 import cli
+
+    for case in golden["cli_gen"]:
+        out = tmp_path / "o.hex"
+        assert cli.main(["gen", "--out", str(out), *case["argv"]]) == 0
+        assert out.read_text() == case["hex"], case["argv"]
+    # raw format == hex format, more lanes than the reference engine is wide
+    raw, hx = tmp_path / "o.bin", tmp_path / "o2.hex"
+    argv = ["--bits", str(200 * 64), "--lanes", "200", "--seed", "ab" * 32]
+    cli.main(["gen", "--format", "raw", "--out", str(raw), *argv])
+    cli.main(["gen", "--out", str(hx), *argv])
+    assert raw.read_bytes().hex() == hx.read_text()
+    first4 = [c for c in golden["cli_gen"] if c["argv"][:4] == ["--bits", "8192", "--lanes", "4"]][0]["hex"]
+    assert raw.read_bytes()[:8].hex() == first4[:16]      # lane 0 of the same seed starts the same way
+    with pytest.raises(SystemExit):
+        cli.main(["gen", "--bits", "12"])
+    with pytest.raises(SystemExit):
+        cli.main(["gen", "--bits", "24", "--lanes", "2"])
+
+
+def test_cli_vectors_and_bench(pkg, tmp_path, capsys):
+    from paper_1909_04750_b200 import cli, vectors
+
+    assert vectors.verify_vectors("mickey") == (3, [])
+    assert cli.main(["vectors"]) == 0
+    f = tmp_path / "v.txt"
+    f.write_text("# comment\nkey=123456789abcdef01234 iv=21436587 ks=9821e10c5ed28d32bbc3d1fb15e93a15\n"
+                 "key=123456789abcdef01234 iv= ks=00f1b8779b47da74075e7a8ccc23c80c\n")
+    assert cli.main(["vectors", "--file", str(f)]) == cli.EXIT_VECTOR_MISMATCH
+    js = tmp_path / "b.json"
+    assert cli.main(["bench", "--mib", "64", "--repeats", "3", "--lanes-log2", "16", "--json-out", str(js)]) == 0
+    import json as _json
+
+    rec = _json.loads(js.read_text())["results"][0]
+    assert {"algorithm", "impl", "width", "nbytes", "seconds", "gbit_per_s", "runs", "speedup_vs_naive"} <= set(rec)
+    assert rec["impl"] == "cuda" and rec["gbit_per_s"] > 10 and len(rec["runs"]) == 3
