@@ -32,6 +32,12 @@ sys.path.insert(0, str(ROOT))
 KEY = bytes.fromhex("123456789abcdef01234")  # eSTREAM vector key (vectors.py:42)
 METRIC = "keystream Tb/s, bitsliced MICKEY 2.0"
 LOP3_PER_CLOCK = 327  # LOP3 per clock per 32-lane word
+# dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the dominant kernel, from the committed
+# `ncu --set full` captures (per launch, like roofline.achieved); only for launches captured exactly.
+NCU_TRAFFIC = {
+    # (layout, instances, clocks): (bytes, source)
+    ("colmajor", 1 << 20, 1_000_000): (131_457_221_000 + 503_661_568, "profiles/r01_ncu_gen_colmajor_c2_full_1Mclk.txt"),
+}
 
 
 def parse_args():
@@ -321,7 +327,9 @@ def run_ours(args):
         "algorithmic_ops_per_launch": lane_ops / max(1, len(gen_events)),
         "avg_launch_ms": kernel_ms_total / max(1, len(gen_events)),
         "kernel_share_of_step": kernel_ms_total / start.elapsed_time(end),
-        "traffic": None,
+        "traffic": NCU_TRAFFIC.get((layout, n, gen_events[0][2] if gen_events else 0), (None, None))[0],
+        "traffic_source": NCU_TRAFFIC.get((layout, n, gen_events[0][2] if gen_events else 0), (None, None))[1],
+        "algorithmic_bytes_per_launch": n * (gen_events[0][2] if gen_events else 0) // 8,
         "hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": hbm_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                 "peak_source": f"MEASURED_PEAKS.json ({peaks_src})", "note": "0.125 B stored per keystream bit; not binding"},

@@ -545,3 +545,22 @@ def test_cli_vectors_and_bench(pkg, tmp_path, capsys):
     rec = _json.loads(js.read_text())["results"][0]
     assert {"algorithm", "impl", "width", "nbytes", "seconds", "gbit_per_s", "runs", "speedup_vs_naive"} <= set(rec)
     assert rec["impl"] == "cuda" and rec["gbit_per_s"] > 10 and len(rec["runs"]) == 3
+
+
+def test_two_threads_two_contexts(pkg, oracle):
+    """One context per worker thread, as the reference's ThreadPoolExecutor bench does (bench.py:265-282)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def work(seed):
+        keys, ivs = random_arrays(seed, 3000)
+        with pkg.MickeyGenerator(0) as gen:
+            col = gen.init_material(keys, ivs, 80).generate_colmajor(700)
+            row = gen.init_material(keys, ivs, 80).generate_rowmajor(512)
+        return seed, col, row
+
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        results = list(pool.map(work, [11, 22, 33, 44]))
+    for seed, col, row in results:
+        keys, ivs = random_arrays(seed, 3000)
+        assert np.array_equal(col, oracle.bulk_colmajor(keys, ivs, 80, 700))
+        assert np.array_equal(row, oracle.bulk_rowmajor(keys, ivs, 80, 512))
