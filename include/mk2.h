@@ -137,6 +137,23 @@ int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_by
  */
 int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n);
 
+/*
+ * Grain v1, the paper's second bitsliced stream cipher (pkg/src/slicerng/grain.py;
+ * compiled loop kernels.py:268-292).  Same context, geometry, layouts, scheduling
+ * and checksum as MICKEY; a context holds the state of one cipher at a time.
+ *   mk2_grain_init_from_material  = GrainSliced.from_key_ivs (grain.py:250-277):
+ *       keys N x 10 bytes, ivs N x 8 bytes, bits LSB-first per byte (grain.py:88-92),
+ *       160 init clocks; lanes N..32G-1 are the reference's unused lanes.
+ *   mk2_grain_generate_colmajor   = kernels.grain_sliced_words (kernels.py:334-342)
+ *   mk2_grain_generate_rowmajor   = lane-major bytes, first bit in the MSB (library
+ *       default) or, with lsb_first != 0, in the LSB (the published vectors' order).
+ *   mk2_grain_state_export        = uint32 bs[160][G]: NFSR words then LFSR words.
+ */
+int mk2_grain_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint64_t N);
+int mk2_grain_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words);
+int mk2_grain_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes, int lsb_first);
+int mk2_grain_state_export(mk2_ctx *ctx, uint32_t *bs);
+
 /* Number of instances / groups / clocks emitted since init. */
 int mk2_query(const mk2_ctx *ctx, uint64_t *N, uint64_t *G, uint64_t *clocks);
 

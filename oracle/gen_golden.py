@@ -256,6 +256,47 @@ def main():
         cli_cases.append({"argv": argv, "hex": out})
     g["cli_gen"] = cli_cases
 
+    # --- Grain v1 (grain.py, kernels.py:268-355): vectors, scalar states, sliced words
+    from slicerng import grain as ref_grain
+
+    gg = {"constants": {k: [list(t) if isinstance(t, tuple) else t for t in v] for k, v in ref_grain.grain_constants().items()
+                        if k != "H_NFSR_TAP"} | {"H_NFSR_TAP": ref_grain.H_NFSR_TAP}}
+    gg["vectors"] = [{"key": r.key.hex(), "iv": r.iv.hex(), "ks": r.ks.hex(), "bit_order": r.bit_order}
+                     for r in ref_vectors.GRAIN_VECTORS]
+    assert ref_vectors.verify_vectors("grain") == (len(ref_vectors.GRAIN_VECTORS), [])
+    R = random.Random(0x6A)
+    sc = []
+    for _ in range(6):
+        m = ref_grain.GrainKeyIv(R.randbytes(10), R.randbytes(8))
+        a = ref_grain.GrainScalar.from_key_iv(m)
+        p = ref_grain.GrainScalarPacked.from_key_iv(m)
+        assert bits_int(a.b) == p.b and bits_int(a.s) == p.s
+        b0, s0 = p.b, p.s                                             # post-init state, before any keystream
+        ks = a.keystream_bytes(128)
+        assert ks == p.keystream_bytes(128)
+        sc.append({"key": m.key.hex(), "iv": m.iv.hex(), "post_init_b": f"{b0:x}", "post_init_s": f"{s0:x}",
+                   "ks128_msb": ks.hex(), "ks64_lsb": ref_grain.GrainScalar.from_key_iv(m).keystream_bytes(64, "lsb").hex()})
+    gg["scalar_cases"] = sc
+    R = random.Random(0xFA57)
+    _ = [R.randbytes(14) for _ in range(64)]                      # skip what test_kernels.py draws for MICKEY
+    gm = [ref_grain.GrainKeyIv(R.randbytes(10), R.randbytes(8)) for _ in range(64)]
+    gcases = []
+    for name, mats, nclk, width in (("w32_7lanes_443", gm[:7], 443, 32), ("w64_64lanes_443", gm, 443, 64),
+                                    ("w32_32lanes_200", gm[:32], 200, 32), ("w64_40lanes_97", gm[:40], 97, 64)):
+        words = ref_kernels.grain_sliced_words(mats, nclk, width)
+        pure = ref_grain.GrainSliced.from_key_ivs(mats, width)
+        st = {"b": [f"{w:x}" for w in pure.b], "s": [f"{w:x}" for w in pure.s]}
+        assert [int(w) for w in words] == pure.keystream_words(nclk)
+        gcases.append({"name": name, "width": width, "nclocks": nclk, "init_state": st,
+                       "materials": [{"key": m.key.hex(), "iv": m.iv.hex()} for m in mats],
+                       "words_hex": words.astype("<u8").tobytes().hex()})
+    gg["sliced_cases"] = gcases
+    words = ref_kernels.grain_sliced_words(gm, 100_000, 64)
+    gg["long"] = {"nclocks": 100_000, "words_u8_sha256": sha(words.astype("<u8").tobytes()),
+                  "lane_major_msb_sha256": sha(ref_kernels.words_lane_major_bytes(words, 64)),
+                  "lane_major_lsb_sha256": sha(ref_kernels.words_lane_major_bytes(words, 64, "lsb"))}
+    g["grain"] = gg
+
     OUT.parent.mkdir(parents=True, exist_ok=True)
     OUT.write_text(json.dumps(g, separators=(",", ":")))
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes)")

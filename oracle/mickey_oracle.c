@@ -558,3 +558,159 @@ void mk2o_derive_material(const uint8_t seed[32], uint32_t tag, uint64_t first_l
         memcpy(ivs + 10 * j, stream + 10, 10);
     }
 }
+
+/* ========================================================================
+ * Grain v1: pkg/src/slicerng/grain.py.
+ * 80-bit NFSR b and 80-bit LFSR s shift together every clock.
+ *   f(s)  = s62^s51^s38^s23^s13^s0                                  grain.py:33-34, 120-124
+ *   g(b)  = 11 linear taps ^ 11 product terms                        grain.py:36-52, 106-117
+ *   h     = 5-input filter over s3,s25,s46,s64,b63                   grain.py:54-56, 96-103
+ *   z     = h ^ b1^b2^b4^b10^b31^b43^b56                             grain.py:58-59, 127-133
+ * init: b = key bits, s = iv bits || 1^16, 160 clocks with z fed back into both
+ * registers (grain.py:147-156); key/IV bits LSB-first per byte (grain.py:88-92).
+ * ====================================================================== */
+#define GB 80
+static const int G_LFSR[6] = {62, 51, 38, 23, 13, 0};
+static const int G_NLIN[11] = {62, 60, 52, 45, 37, 33, 28, 21, 14, 9, 0};
+static const int G_PROD[11][7] = {  /* first entry = length */
+    {2, 63, 60}, {2, 37, 33}, {2, 15, 9}, {3, 60, 52, 45}, {3, 33, 28, 21}, {4, 63, 45, 28, 9},
+    {4, 60, 52, 37, 33}, {4, 63, 60, 21, 15}, {5, 63, 60, 52, 45, 37}, {5, 33, 28, 21, 15, 9},
+    {6, 52, 45, 37, 33, 28, 21}};
+static const int G_OUT[7] = {1, 2, 4, 10, 31, 43, 56};
+
+static inline uint64_t grain_h(uint64_t x0, uint64_t x1, uint64_t x2, uint64_t x3, uint64_t x4)
+{
+    return x1 ^ x4 ^ (x0 & x3) ^ (x2 & x3) ^ (x3 & x4) ^ (x0 & x1 & x2) ^ (x0 & x2 & x3) ^ (x0 & x2 & x4) ^
+           (x1 & x2 & x4) ^ (x2 & x3 & x4);
+}
+static inline uint64_t grain_g(const uint64_t *b)
+{
+    uint64_t v = 0;
+    for (int i = 0; i < 11; ++i) v ^= b[G_NLIN[i]];
+    for (int i = 0; i < 11; ++i) {
+        uint64_t p = ~0ull;
+        for (int k = 1; k <= G_PROD[i][0]; ++k) p &= b[G_PROD[i][k]];
+        v ^= p;
+    }
+    return v;
+}
+static inline uint64_t grain_f(const uint64_t *s)
+{
+    uint64_t v = 0;
+    for (int i = 0; i < 6; ++i) v ^= s[G_LFSR[i]];
+    return v;
+}
+static inline uint64_t grain_z(const uint64_t *b, const uint64_t *s)
+{
+    uint64_t z = grain_h(s[3], s[25], s[46], s[64], b[63]);
+    for (int i = 0; i < 7; ++i) z ^= b[G_OUT[i]];
+    return z;
+}
+
+/* word engine: lanes = bits of the words (1 lane => the scalar engine, GrainScalar grain.py:136-173;
+ * 64 lanes => GrainSliced grain.py:232-308) */
+typedef struct {
+    uint64_t b[GB], s[GB];
+} mk2o_grain;
+
+static void grain_clock(mk2o_grain *st, int init, uint64_t *zout)
+{
+    uint64_t z = grain_z(st->b, st->s);
+    uint64_t fl = grain_f(st->s), fn = grain_g(st->b) ^ st->s[0];
+    if (init) { fl ^= z; fn ^= z; }
+    memmove(st->s, st->s + 1, sizeof(uint64_t) * (GB - 1));
+    memmove(st->b, st->b + 1, sizeof(uint64_t) * (GB - 1));
+    st->s[GB - 1] = fl;
+    st->b[GB - 1] = fn;
+    if (zout) *zout = z;
+}
+
+static inline int lsb_bit(const uint8_t *bytes, int c) { return (bytes[c >> 3] >> (c & 7)) & 1; }
+
+/* GrainSliced.from_key_ivs (grain.py:250-277): keys n x 10, ivs n x 8; the 16 top LFSR words
+ * are ones only in the lanes that exist. */
+int mk2o_grain_init(mk2o_grain *st, const uint8_t *keys, const uint8_t *ivs, int n)
+{
+    if (n < 1 || n > 64) return -1000;
+    memset(st, 0, sizeof *st);
+    for (int j = 0; j < n; ++j) {
+        for (int i = 0; i < 80; ++i) st->b[i] |= (uint64_t)lsb_bit(keys + 10 * j, i) << j;
+        for (int i = 0; i < 64; ++i) st->s[i] |= (uint64_t)lsb_bit(ivs + 8 * j, i) << j;
+    }
+    uint64_t full = n == 64 ? ~0ull : ((1ull << n) - 1);
+    for (int i = 64; i < 80; ++i) st->s[i] = full;
+    for (int c = 0; c < 160; ++c) grain_clock(st, 1, NULL);
+    return 0;
+}
+
+void mk2o_grain_keystream_words(mk2o_grain *st, uint64_t n, uint64_t *out)
+{
+    for (uint64_t t = 0; t < n; ++t) grain_clock(st, 0, &out[t]);
+}
+
+/* bulk layouts as for MICKEY; rowmajor bytes msb (default) or lsb first (grain.py:171-172) */
+typedef struct {
+    const uint8_t *keys, *ivs;
+    uint64_t N, T, G, nb;
+    void *out;
+    int rowmajor, lsb;
+    uint64_t next;
+} grain_job;
+
+static void *grain_worker(void *arg)
+{
+    grain_job *jb = (grain_job *)arg;
+    uint64_t T = jb->T, G = jb->G, rowb = T / 8;
+    uint64_t *words = (uint64_t *)malloc((T + 1) * sizeof(uint64_t));
+    if (!words) return NULL;
+    for (;;) {
+        uint64_t b = __atomic_fetch_add(&jb->next, 1, __ATOMIC_RELAXED);
+        if (b >= jb->nb) break;
+        uint64_t first = b * 64;
+        int n = (int)((jb->N - first) < 64 ? (jb->N - first) : 64);
+        mk2o_grain st;
+        mk2o_grain_init(&st, jb->keys + 10 * first, jb->ivs + 8 * first, n);
+        mk2o_grain_keystream_words(&st, T, words);
+        if (!jb->rowmajor) {
+            uint32_t *out = (uint32_t *)jb->out;
+            for (uint64_t t = 0; t < T; ++t) {
+                out[t * G + 2 * b] = (uint32_t)words[t];
+                if (2 * b + 1 < G) out[t * G + 2 * b + 1] = (uint32_t)(words[t] >> 32);
+            }
+        } else {
+            uint8_t *out = (uint8_t *)jb->out;
+            for (int j = 0; j < n; ++j) {
+                uint8_t *row = out + (first + (uint64_t)j) * rowb;
+                for (uint64_t q = 0; q < rowb; ++q) {
+                    unsigned v = 0;
+                    for (int k = 0; k < 8; ++k) {
+                        unsigned bit = (unsigned)((words[8 * q + k] >> j) & 1);
+                        v |= jb->lsb ? bit << k : bit << (7 - k);
+                    }
+                    row[q] = (uint8_t)v;
+                }
+            }
+        }
+    }
+    free(words);
+    return NULL;
+}
+
+int mk2o_grain_bulk(const uint8_t *keys, const uint8_t *ivs, uint64_t N, uint64_t T, void *out, int rowmajor, int lsb,
+                    int nthreads)
+{
+    if (rowmajor && (T % 8)) return -2;
+    grain_job jb = {keys, ivs, N, T, (N + 31) / 32, (N + 63) / 64, out, rowmajor, lsb, 0};
+    if (nthreads < 1) nthreads = mk2o_max_threads();
+    if ((uint64_t)nthreads > jb.nb) nthreads = (int)(jb.nb ? jb.nb : 1);
+    pthread_t th[1024];
+    if (nthreads > 1024) nthreads = 1024;
+    int started = 0;
+    for (int i = 0; i < nthreads; ++i) {
+        if (pthread_create(&th[i], NULL, grain_worker, &jb) != 0) break;
+        ++started;
+    }
+    if (!started) grain_worker(&jb);
+    for (int i = 0; i < started; ++i) pthread_join(th[i], NULL);
+    return 0;
+}

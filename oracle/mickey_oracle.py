@@ -61,6 +61,11 @@ def lib() -> C.CDLL:
         L.mk2o_checksum_colmajor.restype = C.c_uint64
         L.mk2o_max_threads.restype = C.c_int
         L.mk2o_aes128_encrypt.argtypes = [u8p, u8p, u8p]
+        L.mk2o_grain_init.argtypes = [C.c_void_p, u8p, u8p, C.c_int]
+        L.mk2o_grain_init.restype = C.c_int
+        L.mk2o_grain_keystream_words.argtypes = [C.c_void_p, C.c_uint64, u64p]
+        L.mk2o_grain_bulk.argtypes = [u8p, u8p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_int, C.c_int, C.c_int]
+        L.mk2o_grain_bulk.restype = C.c_int
         L.mk2o_derive_material.argtypes = [u8p, C.c_uint32, C.c_uint64, C.c_uint64, u8p, u8p]
         _lib = L
     return _lib
@@ -282,3 +287,76 @@ def derive_material(seed: bytes, first_lane: int, n: int, tag: int = ALGO_TAG_MI
     ivs = np.zeros((n, 10), np.uint8)
     lib().mk2o_derive_material(_p(sd, u8p), tag, first_lane, n, _p(keys, u8p), _p(ivs, u8p))
     return keys, ivs
+
+
+# ---------------------------------------------------------------- Grain v1 (grain.py)
+
+def _grain_arrays(materials):
+    n = len(materials)
+    keys = np.zeros((n, 10), np.uint8)
+    ivs = np.zeros((n, 8), np.uint8)
+    for j, (key, iv) in enumerate(materials):
+        if len(key) != 10 or len(iv) != 8:
+            raise ValueError(f"lane {j}: key must be 10 bytes and IV 8 bytes")
+        keys[j] = np.frombuffer(bytes(key), np.uint8)
+        ivs[j] = np.frombuffer(bytes(iv), np.uint8)
+    return keys, ivs
+
+
+class GrainSliced:
+    """Up to 64 lanes (restates GrainSliced, grain.py:232-308; 1 lane = GrainScalar :136-173)."""
+
+    def __init__(self):
+        self._st = np.zeros(160, np.uint64)
+
+    @classmethod
+    def from_key_ivs(cls, materials) -> "GrainSliced":
+        keys, ivs = _grain_arrays(materials)
+        st = cls()
+        rc = lib().mk2o_grain_init(st._st.ctypes.data, _p(keys, u8p), _p(ivs, u8p), len(materials))
+        if rc:
+            raise ValueError(f"grain init failed rc={rc}")
+        return st
+
+    @property
+    def b(self):
+        return [int(x) for x in self._st[:80]]
+
+    @property
+    def s(self):
+        return [int(x) for x in self._st[80:]]
+
+    def keystream_words(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.uint64)
+        lib().mk2o_grain_keystream_words(self._st.ctypes.data, n, _p(out, u64p))
+        return out
+
+
+def grain_scalar_bytes(key: bytes, iv: bytes, nbytes: int, bit_order: str = "msb") -> bytes:
+    words = GrainSliced.from_key_ivs([(key, iv)]).keystream_words(8 * nbytes)
+    bits = (words & np.uint64(1)).astype(np.uint8)
+    return np.packbits(bits, bitorder="big" if bit_order == "msb" else "little").tobytes()
+
+
+def grain_bulk_colmajor(keys, ivs, T: int, nthreads: int = 0) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, np.uint8).reshape(-1, 10)
+    ivs = np.ascontiguousarray(ivs, np.uint8).reshape(-1, 8)
+    N = keys.shape[0]
+    out = np.zeros((T, (N + 31) // 32), np.uint32)
+    rc = lib().mk2o_grain_bulk(_p(keys, u8p), _p(ivs, u8p), N, T, out.ctypes.data, 0, 0, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle grain bulk rc={rc}")
+    return out
+
+
+def grain_bulk_rowmajor(keys, ivs, T: int, bit_order: str = "msb", nthreads: int = 0) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, np.uint8).reshape(-1, 10)
+    ivs = np.ascontiguousarray(ivs, np.uint8).reshape(-1, 8)
+    N = keys.shape[0]
+    if T % 8:
+        raise ValueError("bit count must be a multiple of 8")
+    out = np.zeros((N, T // 8), np.uint8)
+    rc = lib().mk2o_grain_bulk(_p(keys, u8p), _p(ivs, u8p), N, T, out.ctypes.data, 1, int(bit_order == "lsb"), nthreads)
+    if rc:
+        raise RuntimeError(f"oracle grain bulk rc={rc}")
+    return out

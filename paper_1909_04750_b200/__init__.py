@@ -6,7 +6,7 @@ lane-major byte layout, served by hand-written sm_100a CUDA kernels behind a
 C ABI (include/mk2.h).  No CPU fallback: importing works anywhere, generating
 needs a B200.
 """
-from . import kernels, mickey, seedgen, sharding
+from . import grain, kernels, mickey, seedgen, sharding
 from .generator import MickeyGenerator
 from .kernels import (
     bulk_colmajor,
@@ -16,6 +16,7 @@ from .kernels import (
     words_to_lane_bits,
     words_to_lane_bytes,
 )
+from .grain import GrainGenerator, GrainKeyIv, GrainKeyIvError, GrainSliced, grain_sliced_words
 from .mickey import MickeyKeyIv, MickeyKeyIvError, MickeySliced, mickey_constants
 from ._native import Mk2Error
 
@@ -23,5 +24,6 @@ __all__ = [
     "MickeyGenerator", "MickeyKeyIv", "MickeyKeyIvError", "MickeySliced", "Mk2Error",
     "mickey_constants", "mickey_sliced_words", "bulk_colmajor", "bulk_rowmajor",
     "words_to_lane_bits", "words_to_lane_bytes", "words_lane_major_bytes",
-    "kernels", "mickey", "seedgen", "sharding",
+    "GrainGenerator", "GrainKeyIv", "GrainKeyIvError", "GrainSliced", "grain_sliced_words",
+    "grain", "kernels", "mickey", "seedgen", "sharding",
 ]

@@ -42,6 +42,10 @@ SYMBOLS = {
     "mk2_init_from_seed": (C.c_int, [_vp, _u8p, _u64, _u64]),
     "mk2_generate_colmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
     "mk2_generate_rowmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
+    "mk2_grain_init_from_material": (C.c_int, [_vp, _u8p, _u8p, _u64]),
+    "mk2_grain_generate_colmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
+    "mk2_grain_generate_rowmajor": (C.c_int, [_vp, _u64, _vp, _u64, C.c_int]),
+    "mk2_grain_state_export": (C.c_int, [_vp, _u32p]),
     "mk2_clock": (C.c_int, [_vp, C.c_int, _u32p, _u64]),
     "mk2_query": (C.c_int, [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "mk2_state_export": (C.c_int, [_vp, _u32p]),

@@ -11,6 +11,7 @@
 
 #include "../../include/mk2.h"
 #include "mk2_kernels.cuh"
+#include "mk2_grain.cuh"
 #include "mk2_seedgen.cuh"
 
 using namespace mk2;
@@ -44,6 +45,8 @@ struct mk2_ctx {
     void *d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     bool ready = false, async = false, timing_open = false;
+    int cipher = 0;        // 0 = MICKEY 2.0, 1 = Grain v1 (which kernels the state belongs to)
+    bool row_lsb = false;  // Grain row-major byte packing of the current call
     float last_ms = 0.f;
     int last_launches = 0;
     int block = BLOCK;  // threads per CTA of the clocking kernels (tunable, <= BLOCK)
@@ -168,6 +171,7 @@ int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bo
     CK(cudaGetLastError());
     ctx->last_launches++;
     ctx->clocks = 0;
+    ctx->cipher = 0;
     ctx->ready = true;
     return MK2_OK;
 }
@@ -205,7 +209,7 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
     // for 256-clock (full 32-byte sector) staging tiles
     p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? (rowmajor ? 224 : 256) : 128);
     p.tg = p.block <= 224 ? 32 : 16;  // strides: <= 128 -> 128, <= 192 -> 192, <= 224 -> 224, else (16, 256)
-    const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : 1u;
+    const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::WIN : 1u);
     auto round_chunk = [&](uint64_t c) {
         c = std::max<uint64_t>(c, granule);
         c = (c + granule - 1) / granule * granule;
@@ -262,6 +266,11 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
     const Plan p = make_plan(ctx, T, false, chains);
     int rc = launch_sched(ctx, p, chains);
     if (rc) return rc;
+    if (ctx->cipher == 1)
+        grain::gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc,
+                                                                        out, stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                                                                        ctx->d_slots, ctx->ring - 1, ctx->d_progress);
+    else
     gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out,
                                                              stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
                                                              ctx->d_slots, ctx->ring - 1, ctx->d_progress, ctx->trace);
@@ -286,11 +295,30 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     gen_rowmajor_kernel<AL, TGV, TSV><<<p.grid, p.block, smem, ctx->stream>>>(                              \
         ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,  \
         ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base)
+#define MK2_GRAIN_ROW_LAUNCH(AL, TGV, TSV, LSBV)                                                              \
+    grain::gen_rowmajor_kernel<AL, TGV, TSV, LSBV><<<p.grid, p.block, smem, ctx->stream>>>(                  \
+        ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,  \
+        ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base)
+#define MK2_GRAIN_ROW_PICK(TGV, TSV)                                                   \
+    do {                                                                               \
+        if (aligned && ctx->row_lsb) MK2_GRAIN_ROW_LAUNCH(true, TGV, TSV, true);       \
+        else if (aligned) MK2_GRAIN_ROW_LAUNCH(true, TGV, TSV, false);                 \
+        else if (ctx->row_lsb) MK2_GRAIN_ROW_LAUNCH(false, TGV, TSV, true);            \
+        else MK2_GRAIN_ROW_LAUNCH(false, TGV, TSV, false);                             \
+    } while (0)
+    if (ctx->cipher == 1) {
+        if (ts == 128) MK2_GRAIN_ROW_PICK(32, 128);
+        else if (ts == 192) MK2_GRAIN_ROW_PICK(32, 192);
+        else if (ts == 224) MK2_GRAIN_ROW_PICK(32, 224);
+        else MK2_GRAIN_ROW_PICK(16, 256);
+    } else
     if (ts == 128) { if (aligned) MK2_ROW_LAUNCH(true, 32, 128); else MK2_ROW_LAUNCH(false, 32, 128); }
     else if (ts == 192) { if (aligned) MK2_ROW_LAUNCH(true, 32, 192); else MK2_ROW_LAUNCH(false, 32, 192); }
     else if (ts == 224) { if (aligned) MK2_ROW_LAUNCH(true, 32, 224); else MK2_ROW_LAUNCH(false, 32, 224); }
     else { if (aligned) MK2_ROW_LAUNCH(true, 16, 256); else MK2_ROW_LAUNCH(false, 16, 256); }
 #undef MK2_ROW_LAUNCH
+#undef MK2_GRAIN_ROW_PICK
+#undef MK2_GRAIN_ROW_LAUNCH
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -394,6 +422,16 @@ int mk2_create(int device, mk2_ctx **out)
     opt_in(gen_rowmajor_kernel<false, 32, 224>);
     opt_in(gen_rowmajor_kernel<true, 16, 256>);
     opt_in(gen_rowmajor_kernel<false, 16, 256>);
+#define MK2_OPT_IN_GRAIN(TGV, TSV)                                  \
+    opt_in(grain::gen_rowmajor_kernel<true, TGV, TSV, true>);       \
+    opt_in(grain::gen_rowmajor_kernel<true, TGV, TSV, false>);      \
+    opt_in(grain::gen_rowmajor_kernel<false, TGV, TSV, true>);      \
+    opt_in(grain::gen_rowmajor_kernel<false, TGV, TSV, false>)
+    MK2_OPT_IN_GRAIN(32, 128);
+    MK2_OPT_IN_GRAIN(32, 192);
+    MK2_OPT_IN_GRAIN(32, 224);
+    MK2_OPT_IN_GRAIN(16, 256);
+#undef MK2_OPT_IN_GRAIN
     if (e != cudaSuccess) {
         std::string msg = std::string("context setup: ") + cudaGetErrorString(e);
         mk2_destroy(c);
@@ -735,7 +773,68 @@ int mk2_init_from_seed(mk2_ctx *ctx, const uint8_t seed[32], uint64_t first_lane
     return end_timing(ctx);
 }
 
+static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words);
+static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes);
+
+static int check_cipher(mk2_ctx *ctx, int cipher)
+{
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    if (ctx->cipher != cipher)
+        return fail(ctx, MK2_E_STATE, cipher ? "context holds MICKEY state: call mk2_grain_init_from_material first"
+                                             : "context holds Grain state: call a MICKEY mk2_init_* first");
+    return MK2_OK;
+}
+
 int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words)
+{
+    int rc = check_cipher(ctx, 0);
+    return rc ? rc : generate_colmajor_impl(ctx, T, out, stride_words);
+}
+
+int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes)
+{
+    int rc = check_cipher(ctx, 0);
+    return rc ? rc : generate_rowmajor_impl(ctx, T, out, pitch_bytes);
+}
+
+int mk2_grain_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint64_t N)
+{
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
+    if (!keys || !ivs) return fail(ctx, MK2_E_ARG, "keys / ivs is NULL");
+    if ((rc = begin_timing(ctx))) return rc;
+    const uint8_t *dk = nullptr, *di = nullptr;
+    void *ok = nullptr, *oi = nullptr;
+    if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
+    if ((rc = stage_input(ctx, ivs, N * 8, &di, &oi))) return rc;
+    grain::init_kernel<<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(dk, di, N, ctx->G, ctx->d_state,
+                                                                                        ctx->d_acc);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    ctx->clocks = 0;
+    ctx->cipher = 1;
+    ctx->ready = true;
+    if (ok) CK(cudaFreeAsync(ok, ctx->stream));
+    if (oi) CK(cudaFreeAsync(oi, ctx->stream));
+    return end_timing(ctx);
+}
+
+int mk2_grain_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words)
+{
+    int rc = check_cipher(ctx, 1);
+    return rc ? rc : generate_colmajor_impl(ctx, T, out, stride_words);
+}
+
+int mk2_grain_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes, int lsb_first)
+{
+    int rc = check_cipher(ctx, 1);
+    if (rc) return rc;
+    ctx->row_lsb = lsb_first != 0;
+    return generate_rowmajor_impl(ctx, T, out, pitch_bytes);
+}
+
+static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words)
 {
     int rc = check_ready(ctx);
     if (rc) return rc;
@@ -777,7 +876,7 @@ int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_w
     return end_timing(ctx);
 }
 
-int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes)
+static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes)
 {
     int rc = check_ready(ctx);
     if (rc) return rc;
@@ -834,7 +933,7 @@ int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_by
 
 int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n)
 {
-    int rc = check_ready(ctx);
+    int rc = check_cipher(ctx, 0);
     if (rc) return rc;
     if (n == 0) return MK2_OK;
     if ((rc = begin_timing(ctx))) return rc;
@@ -875,7 +974,20 @@ int mk2_state_import(mk2_ctx *ctx, const uint32_t *rs, uint64_t N)
     CK(cudaMemsetAsync(ctx->d_acc, 0, sizeof(unsigned long long) * ctx->G, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->clocks = 0;
+    ctx->cipher = 0;
     ctx->ready = true;
+    return MK2_OK;
+}
+
+int mk2_grain_state_export(mk2_ctx *ctx, uint32_t *bs)
+{
+    int rc = check_cipher(ctx, 1);
+    if (rc) return rc;
+    if (!bs) return fail(ctx, MK2_E_ARG, "bs is NULL");
+    const size_t bytes = sizeof(uint32_t) * 2 * grain::GB * ctx->G;
+    CK(cudaMemcpyAsync(bs, ctx->d_state, bytes, is_device_ptr(bs) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return MK2_OK;
 }
 

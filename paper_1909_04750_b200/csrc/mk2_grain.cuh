@@ -1,0 +1,270 @@
+// mk2_grain.cuh -- bitsliced Grain v1 (the paper's second stream cipher).
+//
+// Reference: pkg/src/slicerng/grain.py (engines), kernels.py:268-292 (compiled sliding-window
+// loop).  One thread = 32 instances: b[i] / s[i] hold bit i of the 80-bit NFSR / LFSR.
+// Both registers shift every clock, so unlike MICKEY the state MOVES: the kernel keeps a
+// sliding window of 80 + WIN words per register in registers, runs WIN clocks against
+// compile-time offsets and then realigns the window with WIN-position moves (the same
+// amortised register swap as the reference's numba loop, kernels.py:268-287).  The moves
+// are plain register copies, which ptxas issues on the otherwise idle FMA pipe, so the
+// ALU pipe only sees the ~40 logic ops of f, g, h and z per clock.
+//
+//   f(s) = s62^s51^s38^s23^s13^s0                      grain.py:33-34
+//   g(b) = 11 linear taps ^ 11 product terms           grain.py:36-52
+//   h    = 5-input filter over s3,s25,s46,s64,b63      grain.py:54-56, 96-103
+//   z    = h ^ b1^b2^b4^b10^b31^b43^b56                grain.py:58-59, 127-133
+//   init: b = key bits, s = IV bits || ones, 160 clocks with z fed back into both (grain.py:147-156);
+//   key / IV bits are taken LSB-first per byte (grain.py:88-92).
+#pragma once
+#include "mk2_kernels.cuh"
+
+namespace mk2 {
+namespace grain {
+
+constexpr int GB = 80;           // bits per register (grain.py:29)
+constexpr int WIN = 16;          // clocks per window realignment
+constexpr int GW = GB + WIN;     // window length
+constexpr int INIT_CLOCKS = 160; // grain.py:30
+
+__device__ __forceinline__ uint32_t h_filter(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t x4)
+{
+    return x1 ^ x4 ^ (x0 & x3) ^ (x2 & x3) ^ (x3 & x4) ^ (x0 & x1 & x2) ^ (x0 & x2 & x3) ^ (x0 & x2 & x4) ^
+           (x1 & x2 & x4) ^ (x2 & x3 & x4);
+}
+
+// One clock at window offset C: returns z, appends the two feedback words at C + 80.
+template <int C, bool INIT>
+__device__ __forceinline__ uint32_t step(uint32_t (&b)[GW], uint32_t (&s)[GW])
+{
+    const uint32_t z = h_filter(s[C + 3], s[C + 25], s[C + 46], s[C + 64], b[C + 63]) ^ b[C + 1] ^ b[C + 2] ^ b[C + 4] ^
+                       b[C + 10] ^ b[C + 31] ^ b[C + 43] ^ b[C + 56];
+    uint32_t fl = s[C + 62] ^ s[C + 51] ^ s[C + 38] ^ s[C + 23] ^ s[C + 13] ^ s[C + 0];
+    uint32_t fn = s[C + 0] ^ b[C + 62] ^ b[C + 60] ^ b[C + 52] ^ b[C + 45] ^ b[C + 37] ^ b[C + 33] ^ b[C + 28] ^ b[C + 21] ^
+                  b[C + 14] ^ b[C + 9] ^ b[C + 0];
+    // product terms of g, with the shared sub-products computed once
+    const uint32_t p6360 = b[C + 63] & b[C + 60], p3733 = b[C + 37] & b[C + 33], p159 = b[C + 15] & b[C + 9];
+    const uint32_t p5245 = b[C + 52] & b[C + 45], p2821 = b[C + 28] & b[C + 21];
+    fn ^= p6360 ^ p3733 ^ p159;
+    fn ^= (b[C + 60] & p5245) ^ (b[C + 33] & p2821) ^ (b[C + 63] & b[C + 45] & b[C + 28] & b[C + 9]);
+    fn ^= (b[C + 60] & b[C + 52] & p3733) ^ (p6360 & b[C + 21] & b[C + 15]) ^ (p6360 & p5245 & b[C + 37]);
+    fn ^= (b[C + 33] & p2821 & p159) ^ (p5245 & p3733 & p2821);
+    if (INIT) {
+        fl ^= z;
+        fn ^= z;
+    }
+    s[C + GB] = fl;
+    b[C + GB] = fn;
+    return z;
+}
+
+template <int N>
+__device__ __forceinline__ void realign(uint32_t (&b)[GW], uint32_t (&s)[GW])
+{
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        b[i] = b[i + N];
+        s[i] = s[i + N];
+    }
+}
+
+template <int Lo, int Hi, class F>
+__device__ __forceinline__ void static_for_up(F &&f)
+{
+    if constexpr (Lo < Hi) {
+        f(std::integral_constant<int, Lo>{});
+        static_for_up<Lo + 1, Hi>(f);
+    }
+}
+
+// state[160][G]: words 0..79 = NFSR, 80..159 = LFSR (same coalesced layout as MICKEY's)
+__device__ __forceinline__ void load_state(const uint32_t *state, const unsigned long long *acc, uint64_t G, uint64_t g,
+                                           uint32_t (&b)[GW], uint32_t (&s)[GW], unsigned long long &a)
+{
+    const uint32_t *p = state + g;
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        b[i] = __ldcg(p);
+        bump(p, G);
+    }
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        s[i] = __ldcg(p);
+        bump(p, G);
+    }
+    a = __ldcg(acc + g);
+}
+__device__ __forceinline__ void store_state(uint32_t *state, unsigned long long *acc, uint64_t G, uint64_t g,
+                                            const uint32_t (&b)[GW], const uint32_t (&s)[GW], unsigned long long a)
+{
+    const uint32_t *p = state + g;
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        __stcg(const_cast<uint32_t *>(p), b[i]);
+        bump(p, G);
+    }
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        __stcg(const_cast<uint32_t *>(p), s[i]);
+        bump(p, G);
+    }
+    st_release_u64(acc + g, a);
+}
+
+// ---------------------------------------------------------------------------
+// Key/IV load + 160 init clocks (GrainSliced.from_key_ivs, grain.py:250-277).  The 32
+// instances' key / IV bytes are transposed straight into the registers that ARE the
+// initial state; the 16 top LFSR words are ones only in lanes that exist.
+// ---------------------------------------------------------------------------
+template <int NBYTES>
+__device__ __forceinline__ void load_bits_lsb(const uint8_t *__restrict__ src, uint64_t first_row, uint64_t N,
+                                              uint32_t *dst /* NBYTES * 8 words */)
+{
+#pragma unroll
+    for (int p = 0; p < NBYTES; ++p) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t row = first_row + 8 * q + k;
+                const uint32_t byte = row < N ? src[row * NBYTES + p] : 0u;
+                v |= byte << (8 * q);
+            }
+            w[k] = v;
+        }
+        transpose8x32(w);  // w[bit] = bit `bit` of byte p across the 32 instances
+#pragma unroll
+        for (int m = 0; m < 8; ++m) dst[8 * p + m] = w[m];  // LSB-first: bit m of byte p is register bit 8p + m
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK, 1)
+init_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__ ivs, uint64_t N, uint64_t G,
+            uint32_t *__restrict__ state, unsigned long long *__restrict__ acc)
+{
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    uint32_t b[GW], s[GW];
+    load_bits_lsb<10>(keys, 32 * g, N, b);
+    load_bits_lsb<8>(ivs, 32 * g, N, s);
+    const uint64_t left = N - 32 * g;
+    const uint32_t lanes = left >= 32 ? 0xFFFFFFFFu : ((1u << left) - 1u);
+#pragma unroll
+    for (int i = 64; i < GB; ++i) s[i] = lanes;
+#pragma unroll 1
+    for (int w = 0; w < INIT_CLOCKS / WIN; ++w) {
+        static_for_up<0, WIN>([&](auto ic) { (void)step<decltype(ic)::value, true>(b, s); });
+        realign<WIN>(b, s);
+    }
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        state[(uint64_t)i * G + g] = b[i];
+        state[(uint64_t)(GB + i) * G + g] = s[i];
+    }
+    acc[g] = 0ull;
+}
+
+// ---------------------------------------------------------------------------
+// Keystream kernels: same persistent chain / chunk scheduler as MICKEY's.  `chunk` is a
+// multiple of WIN (column-major) or of the staging tile (row-major); only the very last
+// chunk of a chain can end in a tail of < WIN clocks, run one clock at a time.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(BLOCK, 1)
+gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
+                    unsigned long long *acc_out, uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T,
+                    uint32_t chunk, uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots, uint32_t mask,
+                    uint32_t *progress)
+{
+    uint32_t chain;
+    while (sched_pop(q, slots, mask, chain)) {
+        const uint32_t k = __ldcg(progress + chain);
+        const uint64_t g = (uint64_t)chain * 32 + (threadIdx.x & 31u);
+        const uint64_t t0 = (uint64_t)k * chunk;
+        const uint64_t tc = T - t0 < chunk ? T - t0 : chunk;
+        if (g < G) {
+            uint32_t b[GW], s[GW];
+            unsigned long long a;
+            load_state(state, acc, G, g, b, s, a);
+            uint32_t *p = out + t0 * stride + g;
+            uint64_t t = 0;
+#pragma unroll 1
+            for (; t + WIN <= tc; t += WIN) {
+                static_for_up<0, WIN>([&](auto ic) {
+                    const uint32_t z = step<decltype(ic)::value, false>(b, s);
+                    *p = z;
+                    p += stride;
+                    acc_add(a, z);
+                });
+                realign<WIN>(b, s);
+            }
+#pragma unroll 1
+            for (; t < tc; ++t) {
+                const uint32_t z = step<0, false>(b, s);
+                *p = z;
+                p += stride;
+                acc_add(a, z);
+                realign<1>(b, s);
+            }
+            store_state(state_out, acc_out, G, g, b, s, a);
+        }
+        sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
+    }
+}
+
+template <bool ALIGNED16, int TG, int TS, bool LSB>
+__global__ void __launch_bounds__(BLOCK, 1)
+gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
+                    unsigned long long *acc_out, uint8_t *__restrict__ out, uint64_t pitch, uint64_t N, uint64_t G,
+                    uint64_t T, uint32_t chunk, uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots,
+                    uint32_t mask, uint32_t *progress, uint32_t chain_base)
+{
+    extern __shared__ uint32_t tile[];  // [8 * TG clocks][TS]
+    constexpr uint32_t ts = TS;
+    uint32_t *col = tile + threadIdx.x;
+    uint32_t chain;
+    while (sched_pop(q, slots, mask, chain)) {
+        const uint32_t k = __ldcg(progress + chain);
+        const uint64_t g = (uint64_t)(chain_base + chain) * 32 + (threadIdx.x & 31u);
+        const uint64_t c0 = (uint64_t)k * chunk;
+        const uint64_t tc = T - c0 < chunk ? T - c0 : chunk;
+        if (g < G) {
+            uint32_t b[GW], s[GW];
+            unsigned long long a;
+            load_state(state, acc, G, g, b, s, a);
+            uint8_t *rows = out + 32 * (g - (uint64_t)chain_base * 32) * pitch + (c0 >> 3);
+            const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;
+#pragma unroll 1
+            for (uint64_t t0 = 0; t0 < tc; t0 += 8 * TG) {
+                const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);  // a multiple of 8
+                uint32_t *zp = col;
+                int t = 0;
+#pragma unroll 1
+                for (; t + WIN <= nclk; t += WIN) {
+                    static_for_up<0, WIN>([&](auto ic) {
+                        constexpr int c = decltype(ic)::value;
+                        const uint32_t z = step<c, false>(b, s);
+                        zp[c * ts] = z;
+                        acc_add(a, z);
+                    });
+                    zp += WIN * ts;
+                    realign<WIN>(b, s);
+                }
+#pragma unroll 1
+                for (; t < nclk; ++t) {
+                    const uint32_t z = step<0, false>(b, s);
+                    *zp = z;
+                    zp += ts;
+                    acc_add(a, z);
+                    realign<1>(b, s);
+                }
+                row_drain<ALIGNED16, TG, TS, LSB>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
+            }
+            store_state(state_out, acc_out, G, g, b, s, a);
+        }
+        sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
+    }
+}
+
+}  // namespace grain
+}  // namespace mk2

@@ -519,6 +519,72 @@ __device__ __forceinline__ void bytes4x4(const uint32_t (&x)[4], uint32_t (&y)[4
     y[3] = prmt(b01, b23, 0x7632);
 }
 
+// Drain of one staging tile (ngrp 8-clock groups of keystream words in the thread's smem
+// column `col`, stride TS) into the instance rows at `dst`.  Shared by every cipher's
+// row-major kernel.  LSB selects the byte packing: first bit in the MSB (library default,
+// bitops.py:20-23) or in the LSB (Grain's published convention, grain.py:13-16).
+template <bool ALIGNED16, int TG, int TS, bool LSB>
+__device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t pitch, int ngrp, uint64_t nrows)
+{
+    constexpr uint32_t ts = TS;
+    // ---- pass 1: bit transposes, in place in the smem column; the next group's 8 words
+    // are fetched while the current group is transposed (a lone warp has nobody else to
+    // hide the LDS latency behind)
+    {
+        uint32_t nx[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) nx[m] = col[m * ts];
+#pragma unroll 1
+        for (int grp = 0; grp < ngrp; ++grp) {
+            uint32_t z[8];
+            uint32_t *gp = col + grp * 8 * ts;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) z[LSB ? m : 7 - m] = nx[m];  // clock m -> bit 7 - m (MSB-first) or m
+            if (grp + 1 < ngrp) {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) nx[m] = gp[(8 + m) * ts];
+            }
+            transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) gp[kk * ts] = z[kk];
+        }
+    }
+    // ---- pass 2: TG bytes (or the tail) per instance row, 16 bytes per store; the two
+    // halves of a 32-byte sector are stored back to back so they merge in L2
+    if (ALIGNED16 && ngrp == TG && nrows == 32) {
+#pragma unroll 1
+        for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll 1
+            for (int half = 0; half < TG / 16; ++half) {
+                uint32_t y[4][4];  // [g4][q]
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                    uint32_t x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[u] = col[((16 * half + 4 * g4 + u) * 8 + kk) * ts];
+                    bytes4x4(x, y[g4]);
+                }
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq)
+                    *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half) =
+                        make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]);
+            }
+        }
+    } else {
+        // ragged edge: short tail, partial last group or unaligned rows
+#pragma unroll 1
+        for (int kk = 0; kk < 8; ++kk)
+#pragma unroll 1
+            for (int grp = 0; grp < ngrp; ++grp) {
+                const uint32_t x = col[(grp * 8 + kk) * ts];
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq)
+                    if ((uint64_t)(8 * qq + kk) < nrows)
+                        dst[(uint64_t)(8 * qq + kk) * pitch + grp] = (uint8_t)(x >> (8 * qq));
+            }
+    }
+}
+
 template <bool ALIGNED16, int TG, int TS>
 __global__ void __launch_bounds__(BLOCK, 1)
 gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
@@ -556,63 +622,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     acc_add(a, z);
                     clock<false, false>(r, s, 0u);
                 }
-                // ---- pass 1: bit transposes, in place in the smem column; the next group's 8 words
-                // are fetched while the current group is transposed (a lone warp has nobody else to
-                // hide the LDS latency behind)
-                {
-                    uint32_t nx[8];
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) nx[m] = col[m * ts];
-#pragma unroll 1
-                    for (int grp = 0; grp < ngrp; ++grp) {
-                        uint32_t z[8];
-                        uint32_t *gp = col + grp * 8 * ts;
-#pragma unroll
-                        for (int m = 0; m < 8; ++m) z[7 - m] = nx[m];  // clock m -> bit 7 - m (MSB-first)
-                        if (grp + 1 < ngrp) {
-#pragma unroll
-                            for (int m = 0; m < 8; ++m) nx[m] = gp[(8 + m) * ts];
-                        }
-                        transpose8x32(z);  // z[k]: byte q = output byte of instance 8 q + k
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) gp[kk * ts] = z[kk];
-                    }
-                }
-                // ---- pass 2: TG bytes (or the tail) per instance row, 16 bytes per store; the two
-                // halves of a 32-byte sector are stored back to back so they merge in L2
-                uint8_t *dst = rows + (t0 >> 3);
-                if (ALIGNED16 && ngrp == TG && nrows == 32) {
-#pragma unroll 1
-                    for (int kk = 0; kk < 8; ++kk) {
-#pragma unroll 1
-                        for (int half = 0; half < TG / 16; ++half) {
-                            uint32_t y[4][4];  // [g4][q]
-#pragma unroll
-                            for (int g4 = 0; g4 < 4; ++g4) {
-                                uint32_t x[4];
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) x[u] = col[((16 * half + 4 * g4 + u) * 8 + kk) * ts];
-                                bytes4x4(x, y[g4]);
-                            }
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half) =
-                                    make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]);
-                        }
-                    }
-                } else {
-                    // ragged edge: short tail, partial last group or unaligned rows
-#pragma unroll 1
-                    for (int kk = 0; kk < 8; ++kk)
-#pragma unroll 1
-                        for (int grp = 0; grp < ngrp; ++grp) {
-                            const uint32_t x = col[(grp * 8 + kk) * ts];
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                if ((uint64_t)(8 * qq + kk) < nrows)
-                                    dst[(uint64_t)(8 * qq + kk) * pitch + grp] = (uint8_t)(x >> (8 * qq));
-                        }
-                }
+                row_drain<ALIGNED16, TG, TS, false>(col, rows + (t0 >> 3), pitch, ngrp, nrows);
             }
             store_state(state_out, acc_out, G, g, r, s, a);
         }

@@ -34,7 +34,12 @@ MICKEY_VECTORS = (
     VectorRecord("mickey", _K, b"", bytes.fromhex("92f1b8779b47da74075e7a8ccc23c80c")),
     VectorRecord("mickey", _K, bytes.fromhex("21436587a9cbed0f2143"), bytes.fromhex("804c60856af63516c8f21827bd81f6be")),
 )
-ALL_VECTORS = {"mickey": MICKEY_VECTORS}
+GRAIN_VECTORS = (  # published Grain v1 vectors, LSB-first convention (vectors.py:62-77)
+    VectorRecord("grain", bytes(10), bytes(8), bytes.fromhex("dee931cf1662a72f77d02b6b6188a8f6"), bit_order="lsb"),
+    VectorRecord("grain", bytes.fromhex("0123456789abcdef1234"), bytes.fromhex("0123456789abcdef"),
+                 bytes.fromhex("7f362bd3f7abae2036642fe0bd2aafad"), bit_order="lsb"),
+)
+ALL_VECTORS = {"mickey": MICKEY_VECTORS, "grain": GRAIN_VECTORS}
 
 
 class VectorMismatch(AssertionError):
@@ -61,19 +66,25 @@ def parse_vector_file(text: str, algo: str = "mickey", bit_order: str = "msb"):
 
 def verify_vectors(algo: str = "mickey", records=None, device: int = 0):
     """(records checked, failure descriptions): every lane at W = 32 and 64 on the GPU."""
-    if algo != "mickey":
+    if algo not in ALL_VECTORS:
         raise ValueError(f"algorithm {algo!r} is not on the GPU path of this package")
-    records = MICKEY_VECTORS if records is None else records
+    from . import grain
+
+    records = ALL_VECTORS[algo] if records is None else records
     failures = []
     for rec in records:
-        m = mickey.MickeyKeyIv(rec.key, rec.iv)
         for width in LANE_CHECK_WIDTHS:
-            eng = mickey.MickeySliced.from_key_ivs([m] * width, width=width, device=device)
+            if algo == "mickey":
+                eng = mickey.MickeySliced.from_key_ivs([mickey.MickeyKeyIv(rec.key, rec.iv)] * width, width=width,
+                                                       device=device)
+            else:
+                eng = grain.GrainSliced.from_key_ivs([grain.GrainKeyIv(rec.key, rec.iv)] * width, width=width,
+                                                     device=device)
             words = np.array(eng.keystream_words(8 * len(rec.ks)), np.uint64)
             for j in range(width):
                 bits = ((words >> np.uint64(j)) & np.uint64(1)).astype(np.uint8)
                 got = np.packbits(bits, bitorder="big" if rec.bit_order == "msb" else "little").tobytes()
                 if got != rec.ks:
-                    failures.append(f"mickey width {width} lane {j}: {rec.format_line()} got {got.hex()}")
+                    failures.append(f"{algo} width {width} lane {j}: {rec.format_line()} got {got.hex()}")
                     break
     return len(records), failures

@@ -564,3 +564,94 @@ def test_two_threads_two_contexts(pkg, oracle):
         keys, ivs = random_arrays(seed, 3000)
         assert np.array_equal(col, oracle.bulk_colmajor(keys, ivs, 80, 700))
         assert np.array_equal(row, oracle.bulk_rowmajor(keys, ivs, 80, 512))
+
+
+# ---------------------------------------------------------------- Grain v1
+
+def test_grain_vectors_and_golden_cases(pkg, golden):
+    from paper_1909_04750_b200 import grain, vectors
+
+    assert vectors.verify_vectors("grain") == (2, [])
+    g = golden["grain"]
+    for c in g["sliced_cases"]:
+        mats = [grain.GrainKeyIv(bytes.fromhex(m["key"]), bytes.fromhex(m["iv"])) for m in c["materials"]]
+        eng = grain.GrainSliced.from_key_ivs(mats, width=c["width"])
+        assert [f"{x:x}" for x in eng.b] == c["init_state"]["b"], c["name"]
+        assert [f"{x:x}" for x in eng.s] == c["init_state"]["s"], c["name"]
+        words = grain.grain_sliced_words(mats, c["nclocks"], c["width"])
+        assert words.astype("<u8").tobytes().hex() == c["words_hex"], c["name"]
+        a = eng.keystream_words(100) + eng.keystream_words(c["nclocks"] - 100) if c["nclocks"] > 100 else eng.keystream_words(c["nclocks"])
+        assert a == [int(w) for w in words]                       # resumable, odd split across windows
+    for c in g["scalar_cases"]:
+        m = grain.GrainKeyIv(bytes.fromhex(c["key"]), bytes.fromhex(c["iv"]))
+        eng = grain.GrainSliced.from_key_ivs([m], width=32)
+        lane = eng.extract_lane(0)
+        assert f"{sum(b << i for i, b in enumerate(lane.r)):x}" == c["post_init_b"]
+        assert f"{sum(b << i for i, b in enumerate(lane.s)):x}" == c["post_init_s"]
+        bits = np.array(eng.keystream_lane_bits(1024)[0], np.uint8)
+        assert np.packbits(bits).tobytes().hex() == c["ks128_msb"]
+    mats = [grain.GrainKeyIv(bytes.fromhex(m["key"]), bytes.fromhex(m["iv"])) for m in g["sliced_cases"][1]["materials"]]
+    keys, ivs = grain.pack_materials(mats, 64)
+    T = g["long"]["nclocks"]
+    with grain.GrainGenerator(0) as gen:
+        assert sha(gen.init_material(keys, ivs).generate_colmajor(T).tobytes()) == g["long"]["words_u8_sha256"]
+        c1 = gen.checksum()
+        assert sha(gen.init_material(keys, ivs).generate_rowmajor(T).tobytes()) == g["long"]["lane_major_msb_sha256"]
+        assert gen.checksum() == c1
+        assert sha(gen.init_material(keys, ivs).generate_rowmajor(T, bit_order="lsb").tobytes()) == g["long"]["lane_major_lsb_sha256"]
+        with pytest.raises(pkg.Mk2Error, match="Grain state"):
+            pkg.MickeyGenerator.generate_colmajor(gen, 8)
+
+
+@pytest.mark.parametrize("block,chunk", [(0, 0), (64, 128), (256, 1 << 30), (128, 400)])
+def test_grain_bulk_vs_oracle(pkg, oracle, block, chunk, torch_cuda):
+    from paper_1909_04750_b200 import grain
+
+    rng = np.random.default_rng(77)
+    N, T = 32 * 70 + 11, 1000
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 8), dtype=np.uint8)
+    with grain.GrainGenerator(0) as gen:
+        gen.set_block_threads(block)
+        gen.set_chunk_clocks(chunk)
+        col = gen.init_material(keys, ivs).generate_colmajor(T)
+        row = gen.init_material(keys, ivs).generate_rowmajor(T)
+        # device buffers, resumed in two calls
+        dk, di = torch_cuda.from_numpy(keys).cuda(), torch_cuda.from_numpy(ivs).cuda()
+        gen.init_material(dk, di)
+        dev = torch_cuda.zeros((N, T // 8), dtype=torch_cuda.uint8, device="cuda")
+        gen.generate_rowmajor(512, dev, byte_offset=0, bit_order="lsb")
+        gen.generate_rowmajor(T - 512, dev, byte_offset=64, bit_order="lsb")
+        torch_cuda.cuda.synchronize()
+    assert np.array_equal(col, oracle.grain_bulk_colmajor(keys, ivs, T))
+    assert np.array_equal(row, oracle.grain_bulk_rowmajor(keys, ivs, T))
+    assert np.array_equal(dev.cpu().numpy(), oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb"))
+
+
+def test_grain_large_sampled(pkg, oracle, torch_cuda):
+    """2^20 Grain instances x 4096 bits: sampled groups vs the oracle, layout-independent checksum."""
+    from paper_1909_04750_b200 import grain
+
+    torch = torch_cuda
+    N, T = 1 << 20, 4096
+    rng = np.random.default_rng(3)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 8), dtype=np.uint8)
+    dk, di = torch.from_numpy(keys).cuda(), torch.from_numpy(ivs).cuda()
+    with grain.GrainGenerator(0) as gen:
+        gen.init_material(dk, di)
+        col = torch.empty((T, N // 32), dtype=torch.int32, device="cuda")
+        gen.generate_colmajor(T, col)
+        torch.cuda.synchronize()
+        assert (int(col.view(torch.int64).sum().item()) % (1 << 64)) == gen.checksum()
+        csum = gen.checksum()
+        gen.init_material(dk, di)
+        rows = torch.empty((N, T // 8), dtype=torch.uint8, device="cuda")
+        gen.generate_rowmajor(T, rows)
+        torch.cuda.synchronize()
+        assert gen.checksum() == csum
+    for g in (0, 777, N // 32 - 2):
+        g &= ~1
+        sl = slice(32 * g, 32 * g + 64)
+        assert np.array_equal(col[:, g:g + 2].cpu().numpy().view(np.uint32), oracle.grain_bulk_colmajor(keys[sl], ivs[sl], T))
+        assert np.array_equal(rows[sl].cpu().numpy(), oracle.grain_bulk_rowmajor(keys[sl], ivs[sl], T))

@@ -155,3 +155,26 @@ def test_master_seed_validation():
         MasterSeed(bytes(range(32)), "mickey", 0)
     assert isinstance(SeedError("x"), ValueError)
     assert MasterSeed(bytes(range(32)), "mickey", 1 << 20).lanes == 1 << 20
+
+
+def test_grain_host_mirror(golden):
+    from paper_1909_04750_b200 import grain
+
+    c = grain.grain_constants()
+    ref = golden["grain"]["constants"]
+    for name in ("LFSR_TAPS", "NFSR_LINEAR_TAPS", "H_LFSR_TAPS", "OUTPUT_TAPS"):
+        assert list(c[name]) == ref[name]
+    assert [list(t) for t in c["NFSR_PRODUCT_TAPS"]] == ref["NFSR_PRODUCT_TAPS"] and c["H_NFSR_TAP"] == ref["H_NFSR_TAP"]
+    with pytest.raises(grain.GrainKeyIvError):
+        grain.GrainKeyIv(bytes(9), bytes(8))
+    with pytest.raises(grain.GrainKeyIvError):
+        grain.GrainKeyIv(bytes(10), bytes(7))
+    m = grain.GrainKeyIv(bytes([0x01] + [0] * 9), bytes([0x80] + [0] * 7))
+    assert m.key_bits()[:8] == [1, 0, 0, 0, 0, 0, 0, 0] and m.iv_bits()[:8] == [0, 0, 0, 0, 0, 0, 0, 1]  # LSB-first
+    with pytest.raises(grain.GrainKeyIvError, match="at least one lane"):
+        grain.pack_materials([], 32)
+    with pytest.raises(grain.GrainKeyIvError, match="exceed width"):
+        grain.pack_materials([m] * 33, 32)
+    src = (ROOT / "paper_1909_04750_b200" / "csrc" / "mk2_grain.cuh").read_text()
+    for term in grain.NFSR_LINEAR_TAPS:
+        assert f"b[C + {term}]" in src

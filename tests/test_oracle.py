@@ -161,3 +161,26 @@ def test_aes_blocks_and_seed_derivation(oracle, golden):
     k2, i2 = oracle.derive_material(bytes.fromhex(golden["seedgen"][1]["seed"]), 40, 10)
     kall, iall = oracle.derive_material(bytes.fromhex(golden["seedgen"][1]["seed"]), 0, 64)
     assert np.array_equal(k2, kall[40:50]) and np.array_equal(i2, iall[40:50])
+
+
+def test_grain_oracle_matches_reference(oracle, golden):
+    g = golden["grain"]
+    for v in g["vectors"]:
+        assert oracle.grain_scalar_bytes(bytes.fromhex(v["key"]), bytes.fromhex(v["iv"]), 16, v["bit_order"]).hex() == v["ks"]
+    for c in g["scalar_cases"]:
+        eng = oracle.GrainSliced.from_key_ivs([(bytes.fromhex(c["key"]), bytes.fromhex(c["iv"]))])
+        assert f"{sum((w & 1) << i for i, w in enumerate(eng.b)):x}" == c["post_init_b"]
+        assert f"{sum((w & 1) << i for i, w in enumerate(eng.s)):x}" == c["post_init_s"]
+        assert oracle.grain_scalar_bytes(bytes.fromhex(c["key"]), bytes.fromhex(c["iv"]), 128).hex() == c["ks128_msb"]
+        assert oracle.grain_scalar_bytes(bytes.fromhex(c["key"]), bytes.fromhex(c["iv"]), 64, "lsb").hex() == c["ks64_lsb"]
+    for c in g["sliced_cases"]:
+        mats = [(bytes.fromhex(m["key"]), bytes.fromhex(m["iv"])) for m in c["materials"]]
+        eng = oracle.GrainSliced.from_key_ivs(mats)
+        assert [f"{x:x}" for x in eng.b] == c["init_state"]["b"] and [f"{x:x}" for x in eng.s] == c["init_state"]["s"]
+        assert eng.keystream_words(c["nclocks"]).astype("<u8").tobytes().hex() == c["words_hex"], c["name"]
+    mats = [(bytes.fromhex(m["key"]), bytes.fromhex(m["iv"])) for m in g["sliced_cases"][1]["materials"]]
+    keys, ivs = oracle._grain_arrays(mats)
+    T = g["long"]["nclocks"]
+    assert sha(oracle.grain_bulk_colmajor(keys, ivs, T).tobytes()) == g["long"]["words_u8_sha256"]
+    assert sha(oracle.grain_bulk_rowmajor(keys, ivs, T).tobytes()) == g["long"]["lane_major_msb_sha256"]
+    assert sha(oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb").tobytes()) == g["long"]["lane_major_lsb_sha256"]
