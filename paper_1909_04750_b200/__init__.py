@@ -17,11 +17,13 @@ from .kernels import (
     words_to_lane_bytes,
 )
 from .grain import GrainGenerator, GrainKeyIv, GrainKeyIvError, GrainSliced, grain_sliced_words
-from .mickey import MickeyKeyIv, MickeyKeyIvError, MickeySliced, mickey_constants
+from .mickey import (MickeyKeyIv, MickeyKeyIvError, MickeyScalar, MickeyScalarPacked, MickeySliced, mickey_constants,
+                     scalar_keystream)
 from ._native import Mk2Error
 
 __all__ = [
-    "MickeyGenerator", "MickeyKeyIv", "MickeyKeyIvError", "MickeySliced", "Mk2Error",
+    "MickeyGenerator", "MickeyKeyIv", "MickeyKeyIvError", "MickeyScalar", "MickeyScalarPacked", "MickeySliced",
+    "Mk2Error", "scalar_keystream",
     "mickey_constants", "mickey_sliced_words", "bulk_colmajor", "bulk_rowmajor",
     "words_to_lane_bits", "words_to_lane_bytes", "words_lane_major_bytes",
     "GrainGenerator", "GrainKeyIv", "GrainKeyIvError", "GrainSliced", "grain_sliced_words",

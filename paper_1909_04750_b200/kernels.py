@@ -54,6 +54,17 @@ def _init(gen, keys, ivs, iv_bits):
         gen.init_ragged(keys, ivs, iv_bits)
 
 
+def mickey_naive_bitwise_bytes(material, nbytes: int, device: int = 0) -> bytes:
+    """Single-instance keystream bytes (kernels.py:203-210).  The reference's "naive" engines are its
+    CPU baselines; the bytes are by definition those of one MICKEY instance, served here by the GPU."""
+    return mickey.MickeyScalar.from_key_iv(material, device).keystream_bytes(nbytes)
+
+
+def mickey_packed_bytes(material, nbytes: int, device: int = 0) -> bytes:
+    """Same stream as mickey_naive_bitwise_bytes (kernels.py:213-229)."""
+    return mickey_naive_bitwise_bytes(material, nbytes, device)
+
+
 # --- lane extraction helpers (kernels.py:600-621) ---------------------------
 
 def words_to_lane_bits(words: np.ndarray, lane: int) -> np.ndarray:

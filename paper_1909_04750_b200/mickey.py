@@ -224,3 +224,67 @@ def _as_u64(out: np.ndarray) -> np.ndarray:
     if out.shape[1] == 2:
         return np.ascontiguousarray(out).view("<u8").reshape(-1)
     return out[:, 0].astype(np.uint64)
+
+
+class MickeyScalar:
+    """Single-instance engine with the reference's interface (mickey.py:101-161).
+
+    The reference's bit-serial class is its CPU oracle; here the one instance is
+    lane 0 of a GPU-resident 32-lane group, so every clock still runs in the
+    CUDA kernels (there is no CPU cipher code in this package).  `r` / `s` are
+    0/1 lists read back from the device.
+    """
+
+    def __init__(self, r=None, s=None, device: int = 0):
+        r = [0] * STATE_BITS if r is None else list(r)
+        s = [0] * STATE_BITS if s is None else list(s)
+        if len(r) != STATE_BITS or len(s) != STATE_BITS:
+            raise ValueError("R and S must be 100 bits each")
+        self._eng = MickeySliced([int(b) & 1 for b in r], [int(b) & 1 for b in s], 32, device=device)
+
+    @classmethod
+    def from_key_iv(cls, material: MickeyKeyIv, device: int = 0) -> "MickeyScalar":
+        """Load IV bits, then key bits, then preclock, all with mixing (mickey.py:141-151)."""
+        self = object.__new__(cls)
+        self._eng = MickeySliced.from_key_ivs([material], width=32, device=device)
+        return self
+
+    @property
+    def r(self) -> list:
+        return self._eng.extract_lane(0).r
+
+    @property
+    def s(self) -> list:
+        return self._eng.extract_lane(0).s
+
+    def clock_kg(self, mixing: bool, input_bit: int) -> None:
+        self._eng.clock_kg(mixing, int(input_bit) & 1)
+
+    def keystream_bits(self, nbits: int) -> list:
+        return [int(w) & 1 for w in self._eng.keystream_words(nbits)]
+
+    def keystream_bytes(self, nbytes: int, bit_order: str = "msb") -> bytes:
+        if bit_order not in ("msb", "lsb"):
+            raise ValueError(f"unknown bit order {bit_order!r}")
+        bits = np.array(self.keystream_bits(8 * nbytes), np.uint8)
+        return np.packbits(bits, bitorder="big" if bit_order == "msb" else "little").tobytes()
+
+
+class MickeyScalarPacked(MickeyScalar):
+    """Same engine with each register exposed as one int (mickey.py:173-227): bit i = register bit i."""
+
+    def __init__(self, r: int = 0, s: int = 0, device: int = 0):
+        super().__init__([(r >> i) & 1 for i in range(STATE_BITS)], [(s >> i) & 1 for i in range(STATE_BITS)], device)
+
+    @property
+    def r(self) -> int:  # type: ignore[override]
+        return sum(b << i for i, b in enumerate(self._eng.extract_lane(0).r))
+
+    @property
+    def s(self) -> int:  # type: ignore[override]
+        return sum(b << i for i, b in enumerate(self._eng.extract_lane(0).s))
+
+
+def scalar_keystream(material: MickeyKeyIv, nbits: int, device: int = 0) -> list:
+    """Convenience: initialise and emit nbits (mickey.py:378-380)."""
+    return MickeyScalar.from_key_iv(material, device).keystream_bits(nbits)

@@ -655,3 +655,32 @@ def test_grain_large_sampled(pkg, oracle, torch_cuda):
         sl = slice(32 * g, 32 * g + 64)
         assert np.array_equal(col[:, g:g + 2].cpu().numpy().view(np.uint32), oracle.grain_bulk_colmajor(keys[sl], ivs[sl], T))
         assert np.array_equal(rows[sl].cpu().numpy(), oracle.grain_bulk_rowmajor(keys[sl], ivs[sl], T))
+
+
+def test_scalar_engine_interface(pkg, golden):
+    """MickeyScalar / MickeyScalarPacked / naive-bytes entry points (mickey.py:101-227, kernels.py:203-229):
+    the reference's test_mickey.py scalar tests, served by lane 0 of a GPU group."""
+    for rec in golden["kats"]:                                           # tests/test_mickey.py:38-41
+        st = pkg.MickeyScalar.from_key_iv(pkg.MickeyKeyIv(bytes.fromhex(rec["key"]), bytes.fromhex(rec["iv"])))
+        assert st.keystream_bytes(16).hex() == rec["ks"]
+    for rec in golden["scalar_cases"][:4] + golden["scalar_cases"][-2:]:
+        m = pkg.MickeyKeyIv(*golden_material(rec))
+        a, b = pkg.MickeyScalar.from_key_iv(m), pkg.MickeyScalarPacked.from_key_iv(m)
+        assert f"{sum(x << i for i, x in enumerate(a.r)):x}" == rec["post_init_r"] and f"{b.s:x}" == rec["post_init_s"]
+        assert a.keystream_bytes(64).hex() == rec["ks256"][:128]
+        assert pkg.kernels.mickey_naive_bitwise_bytes(m, 32).hex() == rec["ks256"][:64]
+        assert pkg.kernels.mickey_packed_bytes(m, 32).hex() == rec["ks256"][:64]
+        assert pkg.scalar_keystream(m, 16) == np.unpackbits(np.frombuffer(bytes.fromhex(rec["ks256"][:4]), np.uint8)).tolist()
+    z = pkg.MickeyScalarPacked()                                          # tests/test_mickey.py:59-66
+    z.clock_kg(False, 0)
+    assert f"{z.r:x}" == golden["zero_state_one_clock"]["r"] and f"{z.s:x}" == golden["zero_state_one_clock"]["s"]
+    k = golden["kats"][0]                                                 # tests/test_mickey.py:76-83
+    st = pkg.MickeyScalarPacked.from_key_iv(pkg.MickeyKeyIv(bytes.fromhex(k["key"]), bytes.fromhex(k["iv"])))
+    for r_hex, s_hex in golden["kat0_state_trace_100"][:12]:
+        st.clock_kg(False, 0)
+        assert f"{st.r:x}" == r_hex and f"{st.s:x}" == s_hex
+    by_bytes = pkg.MickeyScalar.from_key_iv(pkg.MickeyKeyIv(bytes(range(10)), b"\xa5"))   # tests/test_mickey.py:102-108
+    by_bits = pkg.MickeyScalar.from_key_iv(pkg.MickeyKeyIv(bytes(range(10)), [1, 0, 1, 0, 0, 1, 0, 1]))
+    assert by_bytes.r == by_bits.r and by_bytes.s == by_bits.s
+    with pytest.raises(ValueError):
+        pkg.MickeyScalar([0] * 99, [0] * 100)
