@@ -17,7 +17,7 @@
 using namespace mk2;
 
 namespace {
-std::string g_create_error;
+thread_local std::string g_create_error;  // text of this thread's last failed mk2_create
 constexpr size_t STAGE_BYTES = size_t(256) << 20;  // per staging buffer for host outputs
 }  // namespace
 
