@@ -255,6 +255,19 @@ def main():
                 assert fh2.read() == out
         cli_cases.append({"argv": argv, "hex": out})
     g["cli_gen"] = cli_cases
+    gcli = []
+    for argv in (
+        ["--bits", "1024"],
+        ["--bits", "4096", "--lanes", "4", "--seed", "ab" * 32],
+        ["--bits", "128", "--key", "0123456789abcdef1234", "--iv", "0123456789abcdef"],
+        ["--bits", "768", "--key", "00000000000000000000", "--lanes", "3"],
+        ["--bits", "2048", "--lanes", "7", "--interleave", "bit", "--seed", "cd" * 32],
+        ["--bits", "4096", "--lanes", "64", "--interleave", "bit"],
+    ):
+        with tempfile.NamedTemporaryFile("r", suffix=".hex") as fh:
+            assert ref_cli.main(["gen", "--algo", "grain", "--impl", "sliced", "--out", fh.name, *argv]) == 0
+            gcli.append({"argv": argv, "hex": fh.read()})
+    g["cli_gen_grain"] = gcli
 
     # --- Grain v1 (grain.py, kernels.py:268-355): vectors, scalar states, sliced words
     from slicerng import grain as ref_grain

@@ -11,7 +11,8 @@ by default (all of lane 0's bytes, then lane 1's, ...), `--interleave bit` emits
 one output word per clock.  For the same seed / key and lane count the bytes are
 identical to the reference's `--impl sliced` and `--impl naive`; `--lanes` may
 exceed the reference's 64 (then a bit-interleaved clock is ceil(lanes/64) 64-bit
-words).  `--impl` accepts only `cuda`: there is no CPU engine in this package.
+words).  `--impl` accepts only `cuda`: there is no CPU engine in this package.  `--algo grain`
+serves the reference's Grain v1 rows the same way.
 """
 from __future__ import annotations
 
@@ -26,6 +27,7 @@ import numpy as np
 
 from . import vectors
 from .generator import MickeyGenerator
+from .grain import GrainGenerator, GrainKeyIv
 from .mickey import MickeyKeyIv
 
 log = logging.getLogger("paper_1909_04750_b200")
@@ -44,6 +46,22 @@ def _parse_hex(text, nbytes=None, what="value"):
     if nbytes is not None and len(data) != nbytes:
         raise ValueError(f"{what} must be {nbytes} bytes, got {len(data)}")
     return data
+
+
+def _init_grain(gen: GrainGenerator, args):
+    """Grain material as cli._material_for builds it (cli.py:41-54): explicit key/IV (IV defaults to zero)
+    or seed-derived with tag 2 (key = stream[0:10], iv = stream[10:18], seedgen.py:24-29)."""
+    if args.key is not None:
+        m = GrainKeyIv(_parse_hex(args.key, 10, "key"), _parse_hex(args.iv or "00" * 8, 8, "iv"))
+        keys = np.tile(np.frombuffer(m.key, np.uint8), (args.lanes, 1))
+        ivs = np.tile(np.frombuffer(m.iv, np.uint8), (args.lanes, 1))
+    else:
+        seed = _parse_hex(args.seed, 32, "seed")
+        if seed == bytes(32):
+            raise ValueError("all-zero master seed rejected")
+        keys, ivs10 = gen.derive_material(seed, 0, args.lanes, algo_tag=2)
+        ivs = np.ascontiguousarray(ivs10[:, :8])
+    gen.init_material(np.ascontiguousarray(keys), np.ascontiguousarray(ivs))
 
 
 def _init_generator(gen: MickeyGenerator, args, lanes_padded: int):
@@ -77,12 +95,18 @@ def cmd_gen(args) -> int:
     if args.bits > (1 << IV_BUDGET_LOG2):
         log.warning("request exceeds 2**%d bits for one key/IV; rotate material", IV_BUDGET_LOG2)
     lanes64 = (args.lanes + 63) // 64 * 64  # the reference engine is 64 lanes wide
-    with MickeyGenerator(args.device) as gen:
-        _init_generator(gen, args, lanes64)
+    grain_algo = args.algo == "grain"
+    with (GrainGenerator if grain_algo else MickeyGenerator)(args.device) as gen:
+        if grain_algo:
+            _init_grain(gen, args)   # unused lanes of the last group are the reference's unused lanes
+        else:
+            _init_generator(gen, args, lanes64)
         if args.interleave == "bit":
             word_bytes = lanes64 // 8
             nclocks = (nbytes + word_bytes - 1) // word_bytes
-            words = gen.generate_colmajor(nclocks)  # uint32 [nclocks][lanes64 / 32]
+            words = gen.generate_colmajor(nclocks, stride_words=lanes64 // 32) if grain_algo else gen.generate_colmajor(nclocks)
+            if grain_algo and gen.groups < lanes64 // 32:
+                words[:, gen.groups:] = 0
             if args.lanes < lanes64:                # unused lanes read 0 (cli.py:125-126)
                 mask = np.zeros(lanes64, np.uint8)
                 mask[: args.lanes] = 1
@@ -112,15 +136,19 @@ def _emit(data: bytes, args) -> None:
 
 
 def cmd_vectors(args) -> int:
-    records = None
-    if args.file:
-        with open(args.file) as fh:
-            records = vectors.parse_vector_file(fh.read(), "mickey", args.bit_order)
-    checked, failures = vectors.verify_vectors("mickey", records, device=args.device)
-    for f in failures:
-        print(f"MISMATCH {f}")
-    print(f"mickey: {checked} vectors checked, {len(failures)} failures")
-    return EXIT_VECTOR_MISMATCH if failures else EXIT_OK
+    algos = [args.algo] if args.algo else (["mickey"] if args.file else ["mickey", "grain"])
+    bad = 0
+    for algo in algos:
+        records = None
+        if args.file:
+            with open(args.file) as fh:
+                records = vectors.parse_vector_file(fh.read(), algo, args.bit_order)
+        checked, failures = vectors.verify_vectors(algo, records, device=args.device)
+        for f in failures:
+            print(f"MISMATCH {f}")
+        print(f"{algo}: {checked} vectors checked, {len(failures)} failures")
+        bad += len(failures)
+    return EXIT_VECTOR_MISMATCH if bad else EXIT_OK
 
 
 def measure(nbytes: int, lanes: int, warmup: int = 1, repeats: int = 5, device: int = 0) -> dict:
@@ -165,7 +193,7 @@ def build_parser() -> argparse.ArgumentParser:
     sub = p.add_subparsers(dest="command", required=True)
 
     g = sub.add_parser("gen", help="generate keystream bytes")
-    g.add_argument("--algo", choices=("mickey",), default="mickey")
+    g.add_argument("--algo", choices=("mickey", "grain"), default="mickey")
     g.add_argument("--impl", choices=("cuda",), default="cuda")
     g.add_argument("--bits", type=int, required=True)
     g.add_argument("--seed", default="11" * 32, help="256-bit master seed (hex) for lane derivation")
@@ -179,7 +207,7 @@ def build_parser() -> argparse.ArgumentParser:
     g.set_defaults(func=cmd_gen)
 
     v = sub.add_parser("vectors", help="verify embedded or file test vectors on the GPU")
-    v.add_argument("--algo", choices=("mickey",), default="mickey")
+    v.add_argument("--algo", choices=("mickey", "grain"))
     v.add_argument("--file", help="vector file: key=<hex> iv=<hex> ks=<hex>")
     v.add_argument("--bit-order", choices=("msb", "lsb"), default="msb")
     v.set_defaults(func=cmd_vectors)

@@ -713,3 +713,13 @@ def test_c3_instance_count_rowmajor_sampled(pkg, golden, oracle, torch_cuda):
         assert gen.checksum() == c_row
         assert (int(col.view(torch.int64).sum().item()) % (1 << 64)) == c_row
         gen.set_stream(None)
+
+
+def test_cli_gen_grain_matches_reference_cli(pkg, golden, tmp_path):
+    from paper_1909_04750_b200 import cli
+
+    for case in golden["cli_gen_grain"]:
+        out = tmp_path / "g.hex"
+        assert cli.main(["gen", "--algo", "grain", "--out", str(out), *case["argv"]]) == 0
+        assert out.read_text() == case["hex"], case["argv"]
+    assert cli.main(["vectors", "--algo", "grain"]) == 0
