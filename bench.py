@@ -144,8 +144,17 @@ def cpu_sample(seconds: float, threads: int | None = None) -> dict:
     ncalls = max(1, min(4096, int(seconds / max(t1, 1e-3))))
     dt = orc.timed_loops(nclocks, cores, ncalls)
     bits = cores * 64 * nclocks * ncalls
+    # the reference's protocol also quotes one worker (bench.measure(..., workers=1)) and the bit-per-cell
+    # "naive" engine for its speed-up claim: both from the same C port
+    t_one = orc.timed_loops(nclocks, 1, 4)
+    st = orc.Scalar.from_key_iv(KEY, b"\x21\x43\x65\x87")
+    t0 = time.perf_counter()
+    st.keystream_bytes(1 << 16)
+    t_naive = time.perf_counter() - t0
     return {"value": bits / dt / 1e12, "unit": "Tb/s", "cores": cores, "kind": "port",
             "seconds": round(dt, 3),
+            "one_thread_gbit_s": 64 * nclocks * 4 / t_one / 1e9,
+            "naive_one_thread_gbit_s": (1 << 19) / t_naive / 1e9,
             "sample": f"{cores} threads x 64 lanes x {nclocks} clocks x {ncalls} calls, keystream loop only "
                       f"(oracle/mickey_oracle.c port of kernels.py:46-95, gcc -O3 -march=x86-64-v3)"}
 
@@ -169,7 +178,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: 2^{n.bit_length() - 1} instances x {clocks} bits per GPU, {layout} "
                                f"(CPU arm: bounded sample of the same keystream loop)"},
-        "cpu_baseline": {**{k: last[k] for k in ("unit", "cores", "kind", "sample")}, "value": value},
+        "cpu_baseline": {**{k: last[k] for k in ("unit", "cores", "kind", "sample", "one_thread_gbit_s", "naive_one_thread_gbit_s")}, "value": value},
         "e2e": {"value": value, "unit": "Tb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }

@@ -25,7 +25,8 @@ KEEP = [
     "smsp__thread_inst_executed_per_inst_executed.ratio",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-    "lts__t_bytes.sum", "l1tex__t_bytes.sum", "smsp__inst_executed_op_local_ld.sum", "smsp__inst_executed_op_local_st.sum",
+    "lts__t_bytes.sum", "l1tex__t_bytes.sum", "smsp__sass_inst_executed_op_local_ld.sum", "smsp__sass_inst_executed_op_local_st.sum",
+    "smsp__sass_inst_executed_op_global_st.sum", "smsp__sass_inst_executed_op_shared_st.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
     "smsp__inst_executed_op_global_st.sum", "smsp__inst_executed_op_global_ld.sum", "smsp__inst_executed_op_shared_st.sum",
     "smsp__inst_executed_op_shared_ld.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "smsp__average_warp_latency_per_inst_issued.ratio", "smsp__warps_eligible.avg.per_cycle_active",
