@@ -7,7 +7,7 @@
 // compile-time offsets and then realigns the window with WIN-position moves (the same
 // amortised register swap as the reference's numba loop, kernels.py:268-287).  The moves
 // are plain register copies, which ptxas issues on the otherwise idle FMA pipe, so the
-// ALU pipe only sees the ~40 logic ops of f, g, h and z per clock.
+// ALU pipe only sees the 38 LOP3s of f, g, h and z per clock.
 //
 //   f(s) = s62^s51^s38^s23^s13^s0                      grain.py:33-34
 //   g(b) = 11 linear taps ^ 11 product terms           grain.py:36-52
@@ -26,31 +26,61 @@ constexpr int WIN = 16;          // clocks per window realignment
 constexpr int GW = GB + WIN;     // window length
 constexpr int INIT_CLOCKS = 160; // grain.py:30
 
-__device__ __forceinline__ uint32_t h_filter(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t x4)
-{
-    return x1 ^ x4 ^ (x0 & x3) ^ (x2 & x3) ^ (x3 & x4) ^ (x0 & x1 & x2) ^ (x0 & x2 & x3) ^ (x0 & x2 & x4) ^
-           (x1 & x2 & x4) ^ (x2 & x3 & x4);
-}
+// LOP3 truth tables used below (inputs a = 0xF0, b = 0xCC, c = 0xAA).
+constexpr unsigned L_XOR3 = 0x96, L_XOR2 = 0x3C, L_AND2 = 0xC0, L_AND3 = 0x80, L_MAJ = 0xE8;
+constexpr unsigned L_A_XOR_BC = 0x78;    // a ^ (b & c)
+constexpr unsigned L_AXORB_AND_C = 0x28; // (a ^ b) & c
 
 // One clock at window offset C: returns z, appends the two feedback words at C + 80.
+// Hand-mapped onto 3-input LUTs: 38 LOP3 per clock (f 3, z 9, g 26); nvcc's own mapping of the
+// textbook expressions (grain.py:96-117) needed 43.
+//   h = A ^ x2 D with A = x1 ^ x4 ^ t, t = x3 (x0 ^ x4), D = t ^ x3 ^ MAJ(x0, x1, x4)   (Shannon on x2)
+//   g = 12 linear taps ^ P1..P11 with the shared pairs b63b60, b37b33, b15b9, b52b45, b28b21; products
+//       of three or more taps are reduced to a pair and folded in as acc ^ (p & q).
 template <int C, bool INIT>
 __device__ __forceinline__ uint32_t step(uint32_t (&b)[GW], uint32_t (&s)[GW])
 {
-    const uint32_t z = h_filter(s[C + 3], s[C + 25], s[C + 46], s[C + 64], b[C + 63]) ^ b[C + 1] ^ b[C + 2] ^ b[C + 4] ^
-                       b[C + 10] ^ b[C + 31] ^ b[C + 43] ^ b[C + 56];
-    uint32_t fl = s[C + 62] ^ s[C + 51] ^ s[C + 38] ^ s[C + 23] ^ s[C + 13] ^ s[C + 0];
-    uint32_t fn = s[C + 0] ^ b[C + 62] ^ b[C + 60] ^ b[C + 52] ^ b[C + 45] ^ b[C + 37] ^ b[C + 33] ^ b[C + 28] ^ b[C + 21] ^
-                  b[C + 14] ^ b[C + 9] ^ b[C + 0];
-    // product terms of g, with the shared sub-products computed once
-    const uint32_t p6360 = b[C + 63] & b[C + 60], p3733 = b[C + 37] & b[C + 33], p159 = b[C + 15] & b[C + 9];
-    const uint32_t p5245 = b[C + 52] & b[C + 45], p2821 = b[C + 28] & b[C + 21];
-    fn ^= p6360 ^ p3733 ^ p159;
-    fn ^= (b[C + 60] & p5245) ^ (b[C + 33] & p2821) ^ (b[C + 63] & b[C + 45] & b[C + 28] & b[C + 9]);
-    fn ^= (b[C + 60] & b[C + 52] & p3733) ^ (p6360 & b[C + 21] & b[C + 15]) ^ (p6360 & p5245 & b[C + 37]);
-    fn ^= (b[C + 33] & p2821 & p159) ^ (p5245 & p3733 & p2821);
-    if (INIT) {
-        fl ^= z;
-        fn ^= z;
+    // ---- output z (grain.py:127-133)
+    const uint32_t x0 = s[C + 3], x1 = s[C + 25], x2 = s[C + 46], x3 = s[C + 64], x4 = b[C + 63];
+    const uint32_t t = lop3<L_AXORB_AND_C>(x0, x4, x3);
+    const uint32_t m = lop3<L_MAJ>(x0, x1, x4);
+    const uint32_t D = lop3<L_XOR3>(t, x3, m);
+    const uint32_t p1 = lop3<L_XOR3>(b[C + 1], b[C + 2], b[C + 4]);
+    const uint32_t p2 = lop3<L_XOR3>(b[C + 10], b[C + 31], b[C + 43]);
+    const uint32_t p3 = lop3<L_XOR3>(b[C + 56], t, x1);
+    const uint32_t p4 = lop3<L_XOR3>(p1, p2, x4);
+    const uint32_t p5 = lop3<L_A_XOR_BC>(p3, x2, D);
+    const uint32_t z = p4 ^ p5;
+    // ---- LFSR feedback f (grain.py:120-124)
+    const uint32_t f1 = lop3<L_XOR3>(s[C + 62], s[C + 51], s[C + 38]);
+    const uint32_t f2 = lop3<L_XOR3>(s[C + 23], s[C + 13], s[C + 0]);
+    // ---- NFSR feedback g ^ s0 (grain.py:106-117)
+    const uint32_t P1 = b[C + 63] & b[C + 60], P2 = b[C + 37] & b[C + 33], P3 = b[C + 15] & b[C + 9];
+    const uint32_t pa = b[C + 52] & b[C + 45], pc = b[C + 28] & b[C + 21];
+    const uint32_t P5 = b[C + 33] & pc;
+    const uint32_t h6 = lop3<L_AND3>(b[C + 63], b[C + 45], b[C + 28]);
+    const uint32_t h7 = b[C + 60] & b[C + 52], h8 = b[C + 21] & b[C + 15], h9 = P1 & pa, h11 = pa & P2;
+    const uint32_t l1 = lop3<L_XOR3>(s[C + 0], b[C + 62], b[C + 60]);
+    const uint32_t l2 = lop3<L_XOR3>(b[C + 52], b[C + 45], b[C + 37]);
+    const uint32_t l3 = lop3<L_XOR3>(b[C + 33], b[C + 28], b[C + 21]);
+    const uint32_t l4 = lop3<L_XOR3>(b[C + 14], b[C + 9], b[C + 0]);
+    const uint32_t l5 = lop3<L_XOR3>(P1, P2, P3);
+    uint32_t accA = lop3<L_XOR3>(l1, l2, l3);
+    uint32_t accB = lop3<L_XOR3>(l4, l5, P5);
+    accA = lop3<L_A_XOR_BC>(accA, b[C + 60], pa);  // P4  = b60 b52 b45
+    accA = lop3<L_A_XOR_BC>(accA, h6, b[C + 9]);   // P6  = b63 b45 b28 b9
+    accA = lop3<L_A_XOR_BC>(accA, h7, P2);         // P7  = b60 b52 b37 b33
+    accA = lop3<L_A_XOR_BC>(accA, h8, P1);         // P8  = b63 b60 b21 b15
+    accB = lop3<L_A_XOR_BC>(accB, h9, b[C + 37]);  // P9  = b63 b60 b52 b45 b37
+    accB = lop3<L_A_XOR_BC>(accB, P5, P3);         // P10 = b33 b28 b21 b15 b9
+    accB = lop3<L_A_XOR_BC>(accB, h11, pc);        // P11 = b52 b45 b37 b33 b28 b21
+    uint32_t fl, fn;
+    if (INIT) {  // z is fed back into both registers (grain.py:150-155)
+        fl = lop3<L_XOR3>(f1, f2, z);
+        fn = lop3<L_XOR3>(accA, accB, z);
+    } else {
+        fl = f1 ^ f2;
+        fn = accA ^ accB;
     }
     s[C + GB] = fl;
     b[C + GB] = fn;
