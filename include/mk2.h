@@ -58,6 +58,10 @@ int mk2_destroy(mk2_ctx *ctx);
 int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream);
 int mk2_use_own_stream(mk2_ctx *ctx);
 int mk2_sync(mk2_ctx *ctx);
+/* Give scratch memory back to the device: the context keeps its stream-ordered
+ * pool (bit-sliced key/IV words, staged inputs) and its host-output staging
+ * buffers warm between calls; state, checksum and scheduler arrays stay. */
+int mk2_trim(mk2_ctx *ctx);
 const char *mk2_last_error(const mk2_ctx *ctx); /* ctx may be NULL: last create error */
 
 /* Shard bookkeeping: this context holds global groups

@@ -33,6 +33,7 @@ SYMBOLS = {
     "mk2_set_chunk_clocks": (C.c_int, [_vp, C.c_uint32]),
     "mk2_last_plan": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_uint32)]),
     "mk2_sync": (C.c_int, [_vp]),
+    "mk2_trim": (C.c_int, [_vp]),
     "mk2_last_error": (C.c_char_p, [_vp]),
     "mk2_set_group_offset": (C.c_int, [_vp, _u64]),
     "mk2_init_from_material": (C.c_int, [_vp, _u8p, _u8p, C.c_uint32, C.c_uint32, _u64]),

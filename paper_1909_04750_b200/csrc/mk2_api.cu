@@ -1,6 +1,7 @@
 // mk2_api.cu -- C-ABI shim (include/mk2.h) over the sm_100a kernels.
 // Host side only does pointer classification, chunking and launches; all
-// cipher work is in mk2_kernels.cuh.  No CPU fallback exists in this file.
+// cipher work is in mk2_clock.cuh / mk2_kernels.cuh (MICKEY 2.0), mk2_grain.cuh (Grain v1) and
+// mk2_seedgen.cuh (seed derivation).  No CPU fallback exists in this file.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -35,7 +36,7 @@ struct mk2_ctx {
     SchedQueue *d_queue = nullptr;       // persistent-kernel scheduler (mk2_kernels.cuh)
     unsigned long long *d_slots = nullptr;
     uint32_t *d_progress = nullptr;
-    uint32_t ring = 0;                   // ring size (power of two >= chains)
+    uint32_t ring = 0;                   // ring size (power of two >= 2 x chains)
     uint32_t chunk_user = 0;             // user override of clocks per scheduling chunk (0 = automatic)
     int block_user = 0;                  // user override of threads per persistent CTA (0 = automatic)
     int last_plan_block = 0;
@@ -195,7 +196,7 @@ int launch_init(mk2_ctx *ctx, const uint32_t *mat, int load_clocks, int lmax, bo
 // ---------------------------------------------------------------------------
 struct Plan {
     int tg;           // row-major only: 8-clock groups per drain (16 or 32)
-    int block;        // threads per CTA (4, 6 or 8 worker warps), one CTA per SM
+    int block;        // threads per CTA (4, 7 or 8 worker warps unless overridden), one CTA per SM
     uint32_t chunk;   // clocks per chunk
     uint32_t cpc;     // chunks per chain
     unsigned grid;
@@ -271,9 +272,9 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
                                                                         out, stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
                                                                         ctx->d_slots, ctx->ring - 1, ctx->d_progress);
     else
-    gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out,
-                                                             stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
-                                                             ctx->d_slots, ctx->ring - 1, ctx->d_progress, ctx->trace);
+        gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out,
+                                                                 stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                                                                 ctx->d_slots, ctx->ring - 1, ctx->d_progress, ctx->trace);
     CK(cudaGetLastError());
     ctx->last_launches++;
     return MK2_OK;
@@ -287,7 +288,7 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     const Plan p = make_plan(ctx, T, true, nchains);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
-    // staging geometry: (TG, stride) = (32, 128) | (32, 192) | (16, 256); the stride is a template
+    // staging geometry: (TG, stride) = (32, 128) | (32, 192) | (32, 224) | (16, 256); the stride is a template
     // parameter so that every smem offset in the drain loops is an immediate
     const int ts = p.tg == 32 ? (p.block <= 128 ? 128 : p.block <= 192 ? 192 : 224) : 256;
     const size_t smem = (size_t)row_smem_bytes(p.tg, ts);
@@ -311,11 +312,15 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
         else if (ts == 192) MK2_GRAIN_ROW_PICK(32, 192);
         else if (ts == 224) MK2_GRAIN_ROW_PICK(32, 224);
         else MK2_GRAIN_ROW_PICK(16, 256);
-    } else
-    if (ts == 128) { if (aligned) MK2_ROW_LAUNCH(true, 32, 128); else MK2_ROW_LAUNCH(false, 32, 128); }
-    else if (ts == 192) { if (aligned) MK2_ROW_LAUNCH(true, 32, 192); else MK2_ROW_LAUNCH(false, 32, 192); }
-    else if (ts == 224) { if (aligned) MK2_ROW_LAUNCH(true, 32, 224); else MK2_ROW_LAUNCH(false, 32, 224); }
-    else { if (aligned) MK2_ROW_LAUNCH(true, 16, 256); else MK2_ROW_LAUNCH(false, 16, 256); }
+    } else if (ts == 128) {
+        if (aligned) MK2_ROW_LAUNCH(true, 32, 128); else MK2_ROW_LAUNCH(false, 32, 128);
+    } else if (ts == 192) {
+        if (aligned) MK2_ROW_LAUNCH(true, 32, 192); else MK2_ROW_LAUNCH(false, 32, 192);
+    } else if (ts == 224) {
+        if (aligned) MK2_ROW_LAUNCH(true, 32, 224); else MK2_ROW_LAUNCH(false, 32, 224);
+    } else {
+        if (aligned) MK2_ROW_LAUNCH(true, 16, 256); else MK2_ROW_LAUNCH(false, 16, 256);
+    }
 #undef MK2_ROW_LAUNCH
 #undef MK2_GRAIN_ROW_PICK
 #undef MK2_GRAIN_ROW_LAUNCH
@@ -560,6 +565,22 @@ int mk2_set_async(mk2_ctx *ctx, int async)
 {
     if (!ctx) return MK2_E_ARG;
     ctx->async = async != 0;
+    return MK2_OK;
+}
+
+int mk2_trim(mk2_ctx *ctx)
+{
+    if (!ctx) return MK2_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->copy));
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->d_stage[b]) cudaFree(ctx->d_stage[b]);
+        ctx->d_stage[b] = nullptr;
+        ctx->copy_pending[b] = false;
+    }
+    ctx->stage_bytes = 0;
+    CK(cudaMemPoolTrimTo(ctx->pool, 0));
     return MK2_OK;
 }
 

@@ -119,6 +119,10 @@ class MickeyGenerator:
     def synchronize(self):
         self._ck(self._lib.mk2_sync(self._ctx), "mk2_sync")
 
+    def trim(self):
+        """Release scratch (key/IV staging pool, host-output staging buffers) back to the device."""
+        self._ck(self._lib.mk2_trim(self._ctx), "mk2_trim")
+
     def set_group_offset(self, group_offset: int):
         self._ck(self._lib.mk2_set_group_offset(self._ctx, int(group_offset)), "mk2_set_group_offset")
 

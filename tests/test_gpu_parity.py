@@ -276,6 +276,16 @@ def test_device_buffers_strides_and_chunked_rows(pkg, oracle, torch_cuda):
         assert np.array_equal(host[:, :128], want_c) and not host[:, 128:].any()
 
 
+def test_trim_keeps_state(pkg, oracle):
+    keys, ivs = random_arrays(8, 2048)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.init_material(keys, ivs, 80)
+        a = gen.generate_rowmajor(256)
+        gen.trim()
+        b = gen.generate_rowmajor(256)
+    assert np.array_equal(np.hstack([a, b]), oracle.bulk_rowmajor(keys, ivs, 80, 512))
+
+
 def test_error_paths(pkg):
     gen = pkg.MickeyGenerator(0)
     with pytest.raises(pkg.Mk2Error, match="mk2_init"):
