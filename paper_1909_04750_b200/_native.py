@@ -77,7 +77,10 @@ def lib() -> C.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            path = _build.LIB
+            import os
+
+            override = os.environ.get("MK2_LIB")  # experiments: an alternative build of the same sources
+            path = Path(override) if override else _build.LIB
             if not path.exists():
                 _build.build_native()
             L = C.CDLL(str(path))

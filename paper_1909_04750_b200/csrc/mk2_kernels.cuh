@@ -15,8 +15,13 @@
 
 #include "mk2_clock.cuh"
 
+#ifndef MK2_COL_UNROLL
+#define MK2_COL_UNROLL 1
+#endif
+
 namespace mk2 {
 
+constexpr int COL_UNROLL = MK2_COL_UNROLL;  // clocks per iteration of the column-major loop (build-time experiment knob)
 constexpr int BLOCK = 256;           // 8 warps = 2 per SM sub-partition at 255 regs/thread
 // Row-major staging: TG 8-clock groups per drain = TG bytes per instance row per drain.
 // TG = 32 (256 clocks, a full 32-byte sector per row) needs 1 KiB of shared memory per
@@ -468,7 +473,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             unsigned long long a;
             load_state(state, acc, G, g, r, s, a);
             uint32_t *p = out + t0 * stride + g;
-#pragma unroll 1
+#pragma unroll COL_UNROLL
             for (uint64_t t = 0; t < tc; ++t) {
                 const uint32_t z = keystream_word(r, s);
                 *p = z;
