@@ -770,3 +770,24 @@ def test_randomized_differential(pkg, oracle):
                 want = oracle.bulk_colmajor(keys, ivs, iv_bits, T)
                 assert gen.checksum() == oracle.checksum_colmajor(want)
         assert np.array_equal(got, want), (case, N, T, ragged, row, block, chunk, split)
+
+
+def test_acceptance_thousand_random_instances(pkg, oracle):
+    """The reference's acceptance criterion (tests/test_acceptance.py:103-135): 1000 random MICKEY instances
+    x 10 000 bits, IV length random 0..10 bytes, sliced engine == per-instance scalar streams."""
+    import random
+
+    rng = random.Random(0xACCE)
+    N, T = 1000, 10_000
+    keys = np.frombuffer(rng.randbytes(10 * N), np.uint8).reshape(N, 10).copy()
+    ivs = np.zeros((N, 10), np.uint8)
+    nbits = np.zeros(N, np.uint8)
+    for n in range(N):
+        ln = rng.randrange(0, 11)
+        ivs[n, :ln] = np.frombuffer(rng.randbytes(ln), np.uint8) if ln else 0
+        nbits[n] = 8 * ln
+    got = pkg.bulk_rowmajor(keys, ivs, nbits, T)
+    assert np.array_equal(got, oracle.bulk_rowmajor(keys, ivs, nbits, T))
+    for n in (0, 499, 999):                      # and the bit-serial engine agrees on single instances
+        st = oracle.Scalar.from_key_iv(keys[n].tobytes(), ivs[n, : nbits[n] // 8].tobytes())
+        assert st.keystream_bytes(T // 8) == got[n].tobytes()

@@ -1,0 +1,73 @@
+"""Structural checks on the compiled kernels (no GPU needed: cuobjdump reads the in-tree library).
+
+The reference proves that its sliced clock is branch-free by tracing the Python operators
+(tests/test_structure.py:26-50 with tests/tracing.py).  The GPU analogue is the machine code itself:
+the keystream clock loop must be straight-line LOP3 code -- exactly the algorithmic 327 LOP3 per clock
+(SURVEY.md 8(d)), no data-dependent branch, no predicated instruction, no local-memory (spill) access.
+"""
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_1909_04750_b200 import _native
+
+pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not available")
+
+
+def _kernel_sass(name_part):
+    txt = subprocess.run(["cuobjdump", "-sass", str(_native.library_path())], stdout=subprocess.PIPE, text=True,
+                         check=True).stdout
+    out = {}
+    for chunk in re.split(r"\n\s*Function : ", txt)[1:]:
+        name = chunk.split("\n", 1)[0].strip()
+        if name_part in name:
+            ins = []
+            for line in chunk.splitlines():
+                m = re.match(r"^\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
+                if m:
+                    ins.append((int(m.group(1), 16), m.group(2).strip()))
+            out[name] = ins
+    return out
+
+
+def _innermost_clock_loops(ins, lo_lop3, hi_lop3):
+    loops = []
+    for addr, text in ins:
+        m = re.search(r"BRA.*0x([0-9a-f]+)", text)
+        if m and int(m.group(1), 16) < addr:
+            body = [(a, t) for a, t in ins if int(m.group(1), 16) <= a <= addr]
+            n = sum("LOP3" in t for _, t in body)
+            if lo_lop3 <= n <= hi_lop3:
+                loops.append(body)
+    return loops
+
+
+@pytest.mark.parametrize("kernel", ["mk219gen_colmajor_kernel", "mk219gen_rowmajor_kernelILb1ELi32ELi224E"])
+def test_mickey_clock_loop_is_straight_line_lop3(kernel):
+    kernels = _kernel_sass(kernel)
+    assert kernels, f"{kernel} not found in libmk2.so"
+    for name, ins in kernels.items():
+        loops = _innermost_clock_loops(ins, 320, 340)
+        assert loops, f"no clock loop found in {name}"
+        body = min(loops, key=len)
+        texts = [t for _, t in body]
+        assert sum("LOP3" in t for t in texts) == _native.lib().mk2_lop3_per_clock() == 327
+        branches = [t for t in texts if re.match(r"(@!?U?P\d+\s+)?(BRA|BRX|JMP|CALL|RET|EXIT|BSSY|BSYNC)", t)]
+        assert len(branches) == 1 and "BRA" in branches[0], branches        # only the loop back-edge
+        predicated = [t for t in texts if t.startswith("@") and "BRA" not in t]
+        assert not predicated, predicated                                     # no per-lane predication
+        assert not [t for t in texts if re.search(r"\b(LDL|STL)\b", t)]        # no spills in the loop
+        alu = [t for t in texts if re.match(r"(LOP3|IADD3|SHF|PRMT|LEA|ISETP|SEL|VIADD|IABS|VIMNMX)", t)]
+        assert len(alu) <= 332, len(alu)                                      # <= 5 non-LOP3 ALU-pipe instructions
+
+
+def test_init_and_grain_loops_have_no_spills_or_branches():
+    for part, lo, hi in (("mk211init_kernelILb0E", 320, 340), ("grain19gen_colmajor", 560, 720)):
+        for name, ins in _kernel_sass(part).items():
+            loops = _innermost_clock_loops(ins, lo, hi)
+            assert loops, name
+            texts = [t for _, t in min(loops, key=len)]
+            assert not [t for t in texts if re.search(r"\b(LDL|STL)\b", t)], name
+            assert sum(bool(re.match(r"(@!?U?P\d+\s+)?BRA", t)) for t in texts) == 1, name
