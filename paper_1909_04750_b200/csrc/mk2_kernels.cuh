@@ -15,13 +15,14 @@
 
 #include "mk2_clock.cuh"
 
-#ifndef MK2_COL_UNROLL
-#define MK2_COL_UNROLL 1
+#ifndef MK2_RBLOCK
+#define MK2_RBLOCK 4
 #endif
 
 namespace mk2 {
 
-constexpr int COL_UNROLL = MK2_COL_UNROLL;  // clocks per iteration of the column-major loop (build-time experiment knob)
+// Clocks per clock_block (deferred R reduction, mk2_clock.cuh).  1 = the plain one-clock body.
+constexpr int RBLOCK = MK2_RBLOCK;
 constexpr int BLOCK = 256;           // 8 warps = 2 per SM sub-partition at 255 regs/thread
 // Row-major staging: TG 8-clock groups per drain = TG bytes per instance row per drain.
 // TG = 32 (256 clocks, a full 32-byte sector per row) needs 1 KiB of shared memory per
@@ -59,6 +60,11 @@ __device__ __forceinline__ void transpose8x32(uint32_t (&w)[8])
     swap_stage<1, 0x55555555u>(w[4], w[5]);
     swap_stage<1, 0x55555555u>(w[6], w[7]);
 }
+
+struct NoInput {  // clock_block's input source when no input word is injected
+    template <class KC>
+    __device__ __forceinline__ uint32_t operator()(KC) const { return 0u; }
+};
 
 // ---------------------------------------------------------------------------
 // Material packing: row-major key/IV bytes -> one bitsliced input word per load
@@ -207,6 +213,27 @@ init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_
             for (int i = 0; i < NBITS; ++i) { r[i] &= act; s[i] &= act; }
         }
     }
+    if constexpr (RBLOCK > 1) {
+        // blocks of RBLOCK load clocks (deferred R reduction); the next block's input words are in flight
+        // while this one runs
+        uint32_t nx[RBLOCK];
+        nx[0] = in_next;
+#pragma unroll
+        for (int k = 1; k < RBLOCK; ++k) nx[k] = c + k < load_clocks ? __ldg(p + (uint64_t)k * G) : 0u;
+#pragma unroll 1
+        for (; c + RBLOCK <= load_clocks; c += RBLOCK) {
+            uint32_t cur[RBLOCK];
+            p += (uint64_t)RBLOCK * G;
+#pragma unroll
+            for (int k = 0; k < RBLOCK; ++k) {
+                cur[k] = nx[k];
+                nx[k] = c + RBLOCK + k < load_clocks ? __ldg(p + (uint64_t)k * G) : 0u;
+            }
+            clock_block<RBLOCK, true, true, false>(
+                r, s, [&](auto kc) { return cur[decltype(kc)::value]; }, [](auto, uint32_t) {});
+        }
+        in_next = nx[0];
+    }
 #pragma unroll 1
     for (; c < load_clocks; ++c) {
         const uint32_t in = in_next;
@@ -214,8 +241,16 @@ init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_
         if (c + 1 < load_clocks) in_next = __ldg(p);
         clock<true, true>(r, s, in);
     }
+    {
+        int k = 0;
+        if constexpr (RBLOCK > 1) {
 #pragma unroll 1
-    for (int k = 0; k < PRECLOCKS; ++k) clock<true, false>(r, s, 0u);
+            for (; k + RBLOCK <= PRECLOCKS; k += RBLOCK)
+                clock_block<RBLOCK, true, false, false>(r, s, NoInput{}, [](auto, uint32_t) {});
+        }
+#pragma unroll 1
+        for (; k < PRECLOCKS; ++k) clock<true, false>(r, s, 0u);
+    }
 
     if constexpr (RAGGED) {
         const uint32_t used = mat[(uint64_t)(2 * lmax + KEY_BITS) * G + g];
@@ -261,6 +296,14 @@ clock_kernel(uint32_t *__restrict__ state, const uint32_t *__restrict__ in_words
 __device__ __forceinline__ void acc_add(unsigned long long &acc, uint32_t z)
 {
     asm("mad.wide.u32 %0, %1, 1, %0;" : "+l"(acc) : "r"(z));
+}
+
+// pointer += bytes (a 64-bit IADD is two ALU-pipe instructions; as a mad.wide ptxas puts
+// the high half on the FMA pipe)
+template <class P>
+__device__ __forceinline__ void ptr_add(P *&p, uint32_t bytes)
+{
+    asm("mad.wide.u32 %0, %1, 1, %0;" : "+l"(p) : "r"(bytes));
 }
 
 // ---------------------------------------------------------------------------
@@ -473,11 +516,22 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             unsigned long long a;
             load_state(state, acc, G, g, r, s, a);
             uint32_t *p = out + t0 * stride + g;
-#pragma unroll COL_UNROLL
-            for (uint64_t t = 0; t < tc; ++t) {
+            const uint32_t stride_bytes = (uint32_t)stride * 4u;  // host side guarantees stride < 2^30
+            uint64_t t = 0;
+            if constexpr (RBLOCK > 1) {
+#pragma unroll 1
+                for (; t + RBLOCK <= tc; t += RBLOCK)
+                    clock_block<RBLOCK, false, false, true>(r, s, NoInput{}, [&](auto, uint32_t z) {
+                        *p = z;
+                        ptr_add(p, stride_bytes);
+                        acc_add(a, z);
+                    });
+            }
+#pragma unroll 1
+            for (; t < tc; ++t) {
                 const uint32_t z = keystream_word(r, s);
                 *p = z;
-                p += stride;
+                ptr_add(p, stride_bytes);
                 acc_add(a, z);
                 clock<false, false>(r, s, 0u);
             }
@@ -619,8 +673,19 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);
                 const int ngrp = nclk >> 3;
                 uint32_t *zp = col;
+                int t = 0;
+                if constexpr (RBLOCK > 1) {
 #pragma unroll 1
-                for (int t = 0; t < nclk; ++t) {
+                    for (; t + RBLOCK <= nclk; t += RBLOCK) {
+                        clock_block<RBLOCK, false, false, true>(r, s, NoInput{}, [&](auto kc, uint32_t z) {
+                            zp[decltype(kc)::value * ts] = z;
+                            acc_add(a, z);
+                        });
+                        zp += RBLOCK * ts;
+                    }
+                }
+#pragma unroll 1
+                for (; t < nclk; ++t) {
                     const uint32_t z = keystream_word(r, s);
                     *zp = z;
                     zp += ts;
