@@ -216,6 +216,16 @@ int mk2_lop3_peak(mk2_ctx *ctx, double *lane_ops_per_s, float *ms);
 /* Static facts about the kernels (for DESIGN.md / bench.py): ALU-pipe logic ops
  * per keystream clock per 32-lane word as counted in SURVEY.md 8(d). */
 int mk2_lop3_per_clock(void);
+/* The kernels run the clock in blocks of mk2_rblock(kernel) clocks with R's
+ * feedback reduction deferred to the end of the block (csrc/mk2_clock.cuh);
+ * mk2_lop3_per_block(kernel) is the number of LOP3 a keystream block executes,
+ * so mk2_lop3_per_block / mk2_rblock < mk2_lop3_per_clock.
+ * kernel: 0 = column-major keystream, 1 = row-major keystream, 2 = key/IV load + pre-clock. */
+#define MK2_KERNEL_COLMAJOR 0
+#define MK2_KERNEL_ROWMAJOR 1
+#define MK2_KERNEL_INIT 2
+int mk2_rblock(int kernel);
+int mk2_lop3_per_block(int kernel);
 
 #ifdef __cplusplus
 }

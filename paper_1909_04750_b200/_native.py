@@ -61,6 +61,8 @@ SYMBOLS = {
     "mk2_set_max_ctas": (C.c_int, [_vp, C.c_uint32]),
     "mk2_lop3_peak": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
     "mk2_lop3_per_clock": (C.c_int, []),
+    "mk2_rblock": (C.c_int, [C.c_int]),
+    "mk2_lop3_per_block": (C.c_int, [C.c_int]),
 }
 
 

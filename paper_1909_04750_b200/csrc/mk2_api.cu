@@ -361,6 +361,19 @@ extern "C" {
 int mk2_abi_version(void) { return 1; }
 
 int mk2_lop3_per_clock(void) { return 327; }
+static int rblock_of(int kernel)
+{
+    return kernel == 1 ? mk2::RBLOCK_ROW : kernel == 2 ? mk2::RBLOCK_INIT : mk2::RBLOCK_COL;
+}
+int mk2_rblock(int kernel) { return rblock_of(kernel); }
+int mk2_lop3_per_block(int kernel)
+{
+    // evaluated at compile time from the tables the clock code is generated from
+    static constexpr int count[mk2::MAX_RBLOCK + 1] = {0, 327, mk2::block_lop3_count(2), mk2::block_lop3_count(3),
+                                                       mk2::block_lop3_count(4), mk2::block_lop3_count(5),
+                                                       mk2::block_lop3_count(6)};
+    return count[rblock_of(kernel)];
+}
 
 int mk2_device_count(void)
 {

@@ -20,8 +20,8 @@
 //
 // The header also compiles as plain host C++ (tests/host_clock_check.cpp): the
 // truth tables are then evaluated in software.  That build exists only so the
-// template code can be checked against the oracle without a GPU; the product
-// library never runs it.
+// test suite can check the template code without a GPU; the product library
+// never runs it.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -248,6 +248,40 @@ MK2_HD uint32_t r_tap(uint32_t x, const uint32_t (&r)[NBITS], const uint32_t (&o
     return v;
 }
 
+// LOP3 count of one keystream clock_block<K> (no input, no mixing, z emitted), from the same
+// tables the code is generated from: the figure bench.py's roofline uses and
+// tests/test_structure.py compares with the SASS.
+MK2_CX int xor_ops(int n) { return n / 2; }  // XOR of n >= 2 words with 3-input LUTs
+MK2_CX int pending(int tap, int k)
+{
+    int n = 0;
+    for (int j = 0; j < k; ++j) n += qbit(j, tap) ? 1 : 0;
+    return n;
+}
+MK2_CX int block_lop3_count(int K)
+{
+    int ops = 0;
+    for (int k = 0; k < K; ++k) {
+        ops += xor_ops(2 + pending(0, k));                                            // z
+        ops += xor_ops(2 + pending(CTRL_R_R_TAP, k));                                 // ctrl_r
+        ops += pending(CTRL_S_R_TAP, k) ? xor_ops(2 + pending(CTRL_S_R_TAP, k)) : 0;  // ctrl_s, else inside fb0 / fb1
+        ops += 2;                                                                     // fb0, fb1
+        ops += 100 + k;                                                               // R, unreduced
+        ops += 174;                                                                   // S
+    }
+    const int HA = (K + 1) / 2;
+    bool used_a[8] = {}, used_b[8] = {};
+    for (int i = 0; i < NBITS; ++i) {
+        const unsigned ma = qmask(i, 0, HA), mb = qmask(i, HA, K);
+        if (ma | mb) ++ops;  // one XOR (or XOR3) per position with pending overflow
+        used_a[ma] = true;
+        used_b[mb] = true;
+    }
+    for (int m = 3; m < 8; ++m)
+        if (m != 4) ops += (used_a[m] ? 1 : 0) + (used_b[m] ? 1 : 0);  // multi-word combinations
+    return ops;
+}
+
 // K x CLOCK_KG.  in_word(k) supplies clock k's input word (INPUT), emit(k, z) receives
 // z = r0 ^ s0 sampled before clock k (EMIT).  Reduced state in, reduced state out.
 template <int K, bool MIXING, bool INPUT, bool EMIT, class In, class Emit>
@@ -259,14 +293,20 @@ MK2_HD void clock_block(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word
         constexpr int k = decltype(kc)::value;
         if constexpr (EMIT) emit(kc, r_tap<0, k, K>(s[0], r, o));
         const uint32_t ctrl_r = r_tap<CTRL_R_R_TAP, k, K>(s[CTRL_R_S_TAP], r, o);
-        const uint32_t ctrl_s = r_tap<CTRL_S_R_TAP, k, K>(s[CTRL_S_S_TAP], r, o);
         [[maybe_unused]] uint32_t in = 0u;
         if constexpr (INPUT) in = in_word(kc);
         uint32_t fb_s;
         if constexpr (INPUT) fb_s = s[99] ^ in;
         else fb_s = s[99];
-        const uint32_t fb1 = fb_s & ctrl_s;
-        const uint32_t fb0 = fb_s & ~ctrl_s;
+        uint32_t fb0, fb1;
+        if constexpr (pending(CTRL_S_R_TAP, k) == 0) {  // ctrl_s = s67 ^ r33 folds into the two masks
+            fb1 = lop3<(LA & (LB ^ LC)) & 0xFF>(fb_s, s[CTRL_S_S_TAP], r[CTRL_S_R_TAP]);
+            fb0 = lop3<(LA & ~(LB ^ LC)) & 0xFF>(fb_s, s[CTRL_S_S_TAP], r[CTRL_S_R_TAP]);
+        } else {
+            const uint32_t ctrl_s = r_tap<CTRL_S_R_TAP, k, K>(s[CTRL_S_S_TAP], r, o);
+            fb1 = fb_s & ctrl_s;
+            fb0 = fb_s & ~ctrl_s;
+        }
 
         // ---- R, unreduced: a'[i] = a[i-1] ^ (ctrl_r & a[i]), a = r[0..99] o[0..k-1]; in_r enters at x^100
         uint32_t top = r[99];  // a[99] ^ in_r: what moves into position 100

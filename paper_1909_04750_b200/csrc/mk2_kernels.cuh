@@ -15,14 +15,26 @@
 
 #include "mk2_clock.cuh"
 
-#ifndef MK2_RBLOCK
-#define MK2_RBLOCK 4
+#ifndef MK2_RBLOCK_COL
+#define MK2_RBLOCK_COL 6
+#endif
+#ifndef MK2_RBLOCK_ROW
+#define MK2_RBLOCK_ROW 5
+#endif
+#ifndef MK2_RBLOCK_INIT
+#define MK2_RBLOCK_INIT 4
 #endif
 
 namespace mk2 {
 
-// Clocks per clock_block (deferred R reduction, mk2_clock.cuh).  1 = the plain one-clock body.
-constexpr int RBLOCK = MK2_RBLOCK;
+// Clocks per clock_block (deferred R reduction, mk2_clock.cuh) in the column-major, row-major and
+// init kernels.  1 = the plain one-clock body.  Build-time knobs: the longer the block, the fewer
+// LOP3 per clock (4: 303.8, 5: 301.2, 6: 299.7) and the larger the loop body (4.9 KB per clock).
+// Defaults from the A/B on B200 (profiles/r01b_probe_rblock.txt): column-major gains up to 6;
+// row-major and init start spilling inside the block at 6 / 5.
+constexpr int RBLOCK_COL = MK2_RBLOCK_COL;
+constexpr int RBLOCK_ROW = MK2_RBLOCK_ROW;
+constexpr int RBLOCK_INIT = MK2_RBLOCK_INIT;
 constexpr int BLOCK = 256;           // 8 warps = 2 per SM sub-partition at 255 regs/thread
 // Row-major staging: TG 8-clock groups per drain = TG bytes per instance row per drain.
 // TG = 32 (256 clocks, a full 32-byte sector per row) needs 1 KiB of shared memory per
@@ -213,23 +225,23 @@ init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_
             for (int i = 0; i < NBITS; ++i) { r[i] &= act; s[i] &= act; }
         }
     }
-    if constexpr (RBLOCK > 1) {
-        // blocks of RBLOCK load clocks (deferred R reduction); the next block's input words are in flight
+    if constexpr (RBLOCK_INIT > 1) {
+        // blocks of RBLOCK_INIT load clocks (deferred R reduction); the next block's input words are in flight
         // while this one runs
-        uint32_t nx[RBLOCK];
+        uint32_t nx[RBLOCK_INIT];
         nx[0] = in_next;
 #pragma unroll
-        for (int k = 1; k < RBLOCK; ++k) nx[k] = c + k < load_clocks ? __ldg(p + (uint64_t)k * G) : 0u;
+        for (int k = 1; k < RBLOCK_INIT; ++k) nx[k] = c + k < load_clocks ? __ldg(p + (uint64_t)k * G) : 0u;
 #pragma unroll 1
-        for (; c + RBLOCK <= load_clocks; c += RBLOCK) {
-            uint32_t cur[RBLOCK];
-            p += (uint64_t)RBLOCK * G;
+        for (; c + RBLOCK_INIT <= load_clocks; c += RBLOCK_INIT) {
+            uint32_t cur[RBLOCK_INIT];
+            p += (uint64_t)RBLOCK_INIT * G;
 #pragma unroll
-            for (int k = 0; k < RBLOCK; ++k) {
+            for (int k = 0; k < RBLOCK_INIT; ++k) {
                 cur[k] = nx[k];
-                nx[k] = c + RBLOCK + k < load_clocks ? __ldg(p + (uint64_t)k * G) : 0u;
+                nx[k] = c + RBLOCK_INIT + k < load_clocks ? __ldg(p + (uint64_t)k * G) : 0u;
             }
-            clock_block<RBLOCK, true, true, false>(
+            clock_block<RBLOCK_INIT, true, true, false>(
                 r, s, [&](auto kc) { return cur[decltype(kc)::value]; }, [](auto, uint32_t) {});
         }
         in_next = nx[0];
@@ -243,10 +255,10 @@ init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_
     }
     {
         int k = 0;
-        if constexpr (RBLOCK > 1) {
+        if constexpr (RBLOCK_INIT > 1) {
 #pragma unroll 1
-            for (; k + RBLOCK <= PRECLOCKS; k += RBLOCK)
-                clock_block<RBLOCK, true, false, false>(r, s, NoInput{}, [](auto, uint32_t) {});
+            for (; k + RBLOCK_INIT <= PRECLOCKS; k += RBLOCK_INIT)
+                clock_block<RBLOCK_INIT, true, false, false>(r, s, NoInput{}, [](auto, uint32_t) {});
         }
 #pragma unroll 1
         for (; k < PRECLOCKS; ++k) clock<true, false>(r, s, 0u);
@@ -297,9 +309,7 @@ __device__ __forceinline__ void acc_add(unsigned long long &acc, uint32_t z)
 {
     asm("mad.wide.u32 %0, %1, 1, %0;" : "+l"(acc) : "r"(z));
 }
-
-// pointer += bytes (a 64-bit IADD is two ALU-pipe instructions; as a mad.wide ptxas puts
-// the high half on the FMA pipe)
+// pointer += bytes: as a mad.wide ptxas puts the carry half on the FMA pipe (IADD3 + IMAD.X)
 template <class P>
 __device__ __forceinline__ void ptr_add(P *&p, uint32_t bytes)
 {
@@ -518,10 +528,10 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             uint32_t *p = out + t0 * stride + g;
             const uint32_t stride_bytes = (uint32_t)stride * 4u;  // host side guarantees stride < 2^30
             uint64_t t = 0;
-            if constexpr (RBLOCK > 1) {
+            if constexpr (RBLOCK_COL > 1) {
 #pragma unroll 1
-                for (; t + RBLOCK <= tc; t += RBLOCK)
-                    clock_block<RBLOCK, false, false, true>(r, s, NoInput{}, [&](auto, uint32_t z) {
+                for (; t + RBLOCK_COL <= tc; t += RBLOCK_COL)
+                    clock_block<RBLOCK_COL, false, false, true>(r, s, NoInput{}, [&](auto, uint32_t z) {
                         *p = z;
                         ptr_add(p, stride_bytes);
                         acc_add(a, z);
@@ -674,14 +684,14 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 const int ngrp = nclk >> 3;
                 uint32_t *zp = col;
                 int t = 0;
-                if constexpr (RBLOCK > 1) {
+                if constexpr (RBLOCK_ROW > 1) {
 #pragma unroll 1
-                    for (; t + RBLOCK <= nclk; t += RBLOCK) {
-                        clock_block<RBLOCK, false, false, true>(r, s, NoInput{}, [&](auto kc, uint32_t z) {
+                    for (; t + RBLOCK_ROW <= nclk; t += RBLOCK_ROW) {
+                        clock_block<RBLOCK_ROW, false, false, true>(r, s, NoInput{}, [&](auto kc, uint32_t z) {
                             zp[decltype(kc)::value * ts] = z;
                             acc_add(a, z);
                         });
-                        zp += RBLOCK * ts;
+                        zp += RBLOCK_ROW * ts;
                     }
                 }
 #pragma unroll 1

@@ -3,7 +3,9 @@
 The reference proves that its sliced clock is branch-free by tracing the Python operators
 (tests/test_structure.py:26-50 with tests/tracing.py).  The GPU analogue is the machine code itself:
 the keystream clock loop must be straight-line LOP3 code -- exactly the algorithmic 327 LOP3 per clock
-(SURVEY.md 8(d)), no data-dependent branch, no predicated instruction, no local-memory (spill) access.
+ in the one-clock body, and the count predicted from the cipher's tables
+(mk2_lop3_per_block: 1794 per 6 clocks = 299 per clock) in the blocked body with R's reduction deferred --
+no data-dependent branch, no predicated instruction, no local-memory (spill) access.
 """
 import re
 import shutil
@@ -61,6 +63,31 @@ def test_mickey_clock_loop_is_straight_line_lop3(kernel):
         assert not [t for t in texts if re.search(r"\b(LDL|STL)\b", t)]        # no spills in the loop
         alu = [t for t in texts if re.match(r"(LOP3|IADD3|SHF|PRMT|LEA|ISETP|SEL|VIADD|IABS|VIMNMX)", t)]
         assert len(alu) <= 332, len(alu)                                      # <= 5 non-LOP3 ALU-pipe instructions
+
+
+@pytest.mark.parametrize("kernel,which", [("mk219gen_colmajor_kernel", 0),
+                                          ("mk219gen_rowmajor_kernelILb1ELi32ELi224E", 1),
+                                          ("mk211init_kernelILb0E", 2)])
+def test_blocked_clock_loop_matches_the_predicted_lop3_count(kernel, which):
+    lib = _native.lib()
+    K, predicted = lib.mk2_rblock(which), lib.mk2_lop3_per_block(which)
+    assert 2 <= K <= 6 and predicted < 327 * K * 0.94          # >= 6% below the one-clock form
+    for name, ins in _kernel_sass(kernel).items():
+        # init runs its blocks with mixing (+ input words): a handful of LOP3 more than the keystream block
+        loops = _innermost_clock_loops(ins, predicted - 2, predicted + 12)
+        assert loops, f"no {K}-clock block loop with ~{predicted} LOP3 in {name}"
+        for body in loops:
+            texts = [t for _, t in body]
+            n = sum("LOP3" in t for t in texts)
+            if which != 2:
+                assert predicted <= n <= predicted + 4, (n, predicted)   # ptxas un-fuses a few XOR3s
+            branches = [t for t in texts if re.match(r"(@!?U?P\d+\s+)?(BRA|BRX|JMP|CALL|RET|EXIT|BSSY|BSYNC)", t)]
+            assert len(branches) == 1 and "BRA" in branches[0], branches
+            if which != 2:                                              # init: the input prefetch is predicated
+                assert not [t for t in texts if t.startswith("@") and "BRA" not in t]
+                assert not [t for t in texts if re.search(r"\b(LDL|STL)\b", t)]
+            alu = [t for t in texts if re.match(r"(LOP3|IADD3|SHF|PRMT|LEA|ISETP|SEL|VIADD|IABS|VIMNMX)", t)]
+            assert len(alu) <= n + 3 * K, (len(alu), n)                 # pointer / checksum adds only
 
 
 def test_init_and_grain_loops_have_no_spills_or_branches():
