@@ -47,13 +47,24 @@ constexpr int row_smem_bytes(int tg, int threads) { return 8 * tg * threads * 4;
 // old bit (8q + b) of w[k]  (four independent 8x8 transposes, one per byte
 // column).  Three half-block swap stages, the log-step scheme of the
 // reference's _square_transpose (pkg/src/slicerng/bitslab.py:183-200)
-// restricted to the last three stages.  2 shifts + 2 LOP3 per pair.
+// restricted to the last three stages.  2 shifts (FMA pipe) + 2 LOP3 per pair.
 // ---------------------------------------------------------------------------
+// Both shifts are issued on the FMA pipe, which the keystream kernels leave idle: the left shift as
+// IMAD.SHL (ptxas' own choice), the right shift as IMAD.HI with the multiplier 2^(32-S) read from
+// constant memory (a literal would be strength-reduced back to an ALU-pipe SHF).  Each merge is ONE
+// LOP3 with the mask as its third operand; written as (x & M) | (y & ~M), ptxas emits two.
+__constant__ uint32_t shr_mul[5] = {0u, 1u << 31, 1u << 30, 0u, 1u << 28};  // [S] = 2^(32-S), S in {1, 2, 4}
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x)
+{
+    return __umulhi(x, shr_mul[S]);
+}
 template <int S, uint32_t M>
 __device__ __forceinline__ void swap_stage(uint32_t &a, uint32_t &b)
 {
-    const uint32_t na = (a & M) | ((b << S) & ~M);
-    const uint32_t nb = ((a >> S) & M) | (b & ~M);
+    constexpr unsigned SEL = ((LA & LC) | (LB & ~LC)) & 0xFF;  // (x & m) | (y & ~m)
+    const uint32_t na = lop3<SEL>(a, b << S, M);
+    const uint32_t nb = lop3<SEL>(shr_fma<S>(a), b, M);
     a = na;
     b = nb;
 }
@@ -309,6 +320,24 @@ __device__ __forceinline__ void acc_add(unsigned long long &acc, uint32_t z)
 {
     asm("mad.wide.u32 %0, %1, 1, %0;" : "+l"(acc) : "r"(z));
 }
+// The same checksum without any ALU-pipe instruction: ptxas re-associates consecutive mad.wide
+// accumulations into 3-input IADD3 + IADD3.X (one ALU slot per clock); integer dot products run on
+// the FMA pipe and are left alone.  Two IDP.2A per keystream word keep the sums of its low and high
+// 16-bit halves in 32-bit registers, exact for up to 65536 words; fold() adds them to the 64-bit sum.
+struct HalfSums {
+    uint32_t lo = 0, hi = 0;
+    __device__ __forceinline__ void add(uint32_t z)
+    {
+        asm("dp2a.lo.u32.u32 %0, %1, %2, %0;" : "+r"(lo) : "r"(z), "r"(0x00000001));  // += z & 0xFFFF
+        asm("dp2a.lo.u32.u32 %0, %1, %2, %0;" : "+r"(hi) : "r"(z), "r"(0x00000100));  // += z >> 16
+    }
+    __device__ __forceinline__ void fold(unsigned long long &acc)
+    {
+        acc += (unsigned long long)lo + ((unsigned long long)hi << 16);
+        lo = hi = 0;
+    }
+};
+constexpr uint32_t HALFSUM_MAX_WORDS = 65536;
 // pointer += bytes: as a mad.wide ptxas puts the carry half on the FMA pipe (IADD3 + IMAD.X)
 template <class P>
 __device__ __forceinline__ void ptr_add(P *&p, uint32_t bytes)
@@ -525,25 +554,58 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             uint32_t r[NBITS], s[NBITS];
             unsigned long long a;
             load_state(state, acc, G, g, r, s, a);
-            uint32_t *p = out + t0 * stride + g;
-            const uint32_t stride_bytes = (uint32_t)stride * 4u;  // host side guarantees stride < 2^30
+#ifndef MK2_COL_ADDR
+#define MK2_COL_ADDR 0
+#endif
+#ifndef MK2_COL_SUM
+#define MK2_COL_SUM 0
+#endif
+            // Build-time experiment knobs (profiles/r01b_probe_col_row_variants.txt).  MK2_COL_ADDR 1: a
+            // 64-bit base and a 32-bit element index (index * 4 + base is one IMAD.WIDE, the index bump a
+            // uniform-datapath IMAD) instead of a 64-bit pointer bump (IADD3 + IMAD.X per clock);
+            // MK2_COL_SUM 1: IDP.2A half sums instead of the mad.wide accumulate (3-input IADD3 + IADD3.X
+            // per two clocks).  Both remove every non-LOP3 instruction from the ALU pipe (1810 -> 1798 per
+            // six clocks) and both are SLOWER by 0.3-0.7% on the B200 in this loop, so the defaults are 0/0;
+            // the row-major loop, with its shared-memory stores, gains 1.5% from the half sums at 2^24 instances.
+            uint32_t *base = out + t0 * stride + g;
+            const uint32_t stride32 = (uint32_t)stride;  // host side guarantees stride < 2^30
+            uint32_t seg_max = 0xFFFFFFFFu / stride32;
+            if (seg_max > HALFSUM_MAX_WORDS) seg_max = HALFSUM_MAX_WORDS;
+            if (seg_max > RBLOCK_COL) seg_max -= seg_max % RBLOCK_COL;
             uint64_t t = 0;
-            if constexpr (RBLOCK_COL > 1) {
 #pragma unroll 1
-                for (; t + RBLOCK_COL <= tc; t += RBLOCK_COL)
-                    clock_block<RBLOCK_COL, false, false, true>(r, s, NoInput{}, [&](auto, uint32_t z) {
-                        *p = z;
-                        ptr_add(p, stride_bytes);
-                        acc_add(a, z);
-                    });
-            }
+            while (t < tc) {
+                const uint32_t nseg = tc - t < seg_max ? (uint32_t)(tc - t) : seg_max;
+                uint32_t idx = 0, u = 0;
+                uint32_t *p = base;
+                HalfSums hs;
+                auto emit = [&](uint32_t z) {
+#if MK2_COL_ADDR
+                    base[idx] = z;
+                    idx += stride32;
+#else
+                    *p = z;
+                    ptr_add(p, stride32 * 4u);
+#endif
+#if MK2_COL_SUM
+                    hs.add(z);
+#else
+                    acc_add(a, z);
+#endif
+                };
+                if constexpr (RBLOCK_COL > 1) {
 #pragma unroll 1
-            for (; t < tc; ++t) {
-                const uint32_t z = keystream_word(r, s);
-                *p = z;
-                ptr_add(p, stride_bytes);
-                acc_add(a, z);
-                clock<false, false>(r, s, 0u);
+                    for (; u + RBLOCK_COL <= nseg; u += RBLOCK_COL)
+                        clock_block<RBLOCK_COL, false, false, true>(r, s, NoInput{}, [&](auto, uint32_t z) { emit(z); });
+                }
+#pragma unroll 1
+                for (; u < nseg; ++u) {
+                    emit(keystream_word(r, s));
+                    clock<false, false>(r, s, 0u);
+                }
+                hs.fold(a);
+                base += (uint64_t)nseg * stride;
+                t += nseg;
             }
             store_state(state_out, acc_out, G, g, r, s, a);
         }
@@ -682,14 +744,22 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             for (uint64_t t0 = 0; t0 < tc; t0 += 8 * TG) {
                 const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);
                 const int ngrp = nclk >> 3;
+#ifndef MK2_ROW_SUM
+#define MK2_ROW_SUM 1
+#endif
                 uint32_t *zp = col;
                 int t = 0;
+                HalfSums hs;  // a tile is at most 256 words
                 if constexpr (RBLOCK_ROW > 1) {
 #pragma unroll 1
                     for (; t + RBLOCK_ROW <= nclk; t += RBLOCK_ROW) {
                         clock_block<RBLOCK_ROW, false, false, true>(r, s, NoInput{}, [&](auto kc, uint32_t z) {
                             zp[decltype(kc)::value * ts] = z;
+#if MK2_ROW_SUM
+                            hs.add(z);
+#else
                             acc_add(a, z);
+#endif
                         });
                         zp += RBLOCK_ROW * ts;
                     }
@@ -699,9 +769,14 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     const uint32_t z = keystream_word(r, s);
                     *zp = z;
                     zp += ts;
+#if MK2_ROW_SUM
+                    hs.add(z);
+#else
                     acc_add(a, z);
+#endif
                     clock<false, false>(r, s, 0u);
                 }
+                hs.fold(a);
                 row_drain<ALIGNED16, TG, TS, false>(col, rows + (t0 >> 3), pitch, ngrp, nrows);
             }
             store_state(state_out, acc_out, G, g, r, s, a);

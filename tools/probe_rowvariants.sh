@@ -1,0 +1,7 @@
+#!/bin/bash
+for rep in 1 2 3; do
+for lib in "" variants/libmk2_rs1.so; do
+  echo "== rep $rep lib=${lib:-default(row sum = mad.wide)}"
+  MK2_LIB=$lib python tools/probe_one.py row 22 16384 0 0 2>&1 | tail -1
+  MK2_LIB=$lib python tools/probe_one.py row 24 8192 0 0 2>&1 | tail -1
+done; done
