@@ -191,6 +191,10 @@ int mk2_set_async(mk2_ctx *ctx, int async);
  * its state and goes back to the ready queue.
  * mk2_last_plan reports what the most recent keystream launch used. */
 int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
+/* Tuning knob: size of one device staging tile for HOST output buffers (two are
+ * in flight: one being generated, one being copied out).  0 = default (32 MiB;
+ * row-major tiles, which are 2-D copies, are 16x this). */
+int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes);
 int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 
 /* Diagnostics: per-job trace of the column-major persistent kernel.  Records

@@ -19,7 +19,12 @@ using namespace mk2;
 
 namespace {
 thread_local std::string g_create_error;  // text of this thread's last failed mk2_create
-constexpr size_t STAGE_BYTES = size_t(256) << 20;  // per staging buffer for host outputs
+// Per staging buffer for host outputs (two in flight).  Column-major tiles are plain 1-D copies: small
+// tiles shorten the pipeline fill (measured on B200, 2 GiB per call: 32 MiB 54.8 GB/s, 256 MiB 53.0 GB/s).
+// Row-major tiles are 2-D copies whose rows must stay >= 512 B wide (64 B rows: 16 GB/s), so they are
+// 16x larger (profiles/r01b_probe_e2e_stage.txt).
+constexpr size_t STAGE_BYTES = size_t(32) << 20;
+constexpr size_t ROW_TILE_FACTOR = 16;
 }  // namespace
 
 struct mk2_ctx {
@@ -39,6 +44,7 @@ struct mk2_ctx {
     uint32_t ring = 0;                   // ring size (power of two >= 2 x chains)
     uint32_t chunk_user = 0;             // user override of clocks per scheduling chunk (0 = automatic)
     int block_user = 0;                  // user override of threads per persistent CTA (0 = automatic)
+    size_t stage_target = STAGE_BYTES;   // bytes per host-output staging tile (mk2_set_stage_bytes)
     int last_plan_block = 0;
     uint32_t last_plan_chunk = 0;
     Trace trace = {nullptr, nullptr, 0}; // optional per-job trace (device buffers owned by the ctx)
@@ -562,6 +568,14 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
     return MK2_OK;
 }
 
+int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (bytes && bytes < (1u << 20)) return fail(ctx, MK2_E_ARG, "stage bytes must be 0 (default) or at least 1 MiB");
+    ctx->stage_target = bytes ? (size_t)bytes : STAGE_BYTES;
+    return MK2_OK;
+}
+
 int mk2_set_block_threads(mk2_ctx *ctx, int threads)
 {
     if (!ctx) return MK2_E_ARG;
@@ -885,7 +899,7 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
         if ((rc = launch_col(ctx, T, static_cast<uint32_t *>(out), stride_words))) return rc;
     } else {
         const size_t row_bytes = ctx->G * sizeof(uint32_t);
-        const size_t want = std::max<size_t>(std::min<size_t>(STAGE_BYTES, T * row_bytes), row_bytes);
+        const size_t want = std::max<size_t>(std::min<size_t>(ctx->stage_target, T * row_bytes), row_bytes);
         if ((rc = ensure_stage(ctx, want))) return rc;
         const uint64_t chunk = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
         int b = 0;
@@ -934,7 +948,7 @@ static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
         // because the time loop is the inner one.
         const uint64_t block_chains = std::min<uint64_t>(chains, 2ull * 8ull * (uint64_t)ctx->sm_count);
         const uint64_t block_rows = block_chains * 1024;
-        uint64_t tc_max = std::max<uint64_t>(256, (size_t(1) << 30) / block_rows / 32 * 256);  // <= 1 GiB per tile
+        uint64_t tc_max = std::max<uint64_t>(256, ROW_TILE_FACTOR * ctx->stage_target / block_rows / 32 * 256);
         tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
         if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
         int b = 0;

@@ -85,6 +85,10 @@ class MickeyGenerator:
         """Tuning knob: clocks per scheduling chunk of the persistent keystream kernels."""
         self._ck(self._lib.mk2_set_chunk_clocks(self._ctx, int(clocks)), "mk2_set_chunk_clocks")
 
+    def set_stage_bytes(self, nbytes: int):
+        """Tuning knob: bytes per device staging tile when the output buffer is in host memory."""
+        self._ck(self._lib.mk2_set_stage_bytes(self._ctx, int(nbytes)), "mk2_set_stage_bytes")
+
     def set_async(self, flag: bool):
         self._ck(self._lib.mk2_set_async(self._ctx, int(bool(flag))), "mk2_set_async")
 
