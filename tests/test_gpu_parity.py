@@ -399,6 +399,29 @@ def test_rowmajor_host_output_tiles(pkg, oracle):
         assert rows[n, : T // 8].tobytes() == oracle.bulk_rowmajor(keys, ivs, 80, T)[0].tobytes(), n
 
 
+@pytest.mark.parametrize("stage_mib", [1, 3])
+def test_host_outputs_with_small_staging_tiles(pkg, oracle, stage_mib):
+    """mk2_set_stage_bytes: host outputs cut into many staging tiles (column-major: time chunks; row-major:
+    [chain block] x [time chunk] 2-D copies) are the same bits as the oracle's."""
+    N, T = 32 * 32 * 9 + 7, 8192 + 264
+    rng = np.random.default_rng(stage_mib)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stage_bytes(stage_mib << 20)
+        gen.init_material(keys, ivs, 80)
+        cols = gen.generate_colmajor(T)
+        c1 = gen.checksum()
+        gen.init_material(keys, ivs, 80)
+        rows = np.zeros((N, T // 8 + 3), np.uint8)
+        gen.generate_rowmajor(T, rows, pitch_bytes=rows.shape[1])
+        assert gen.checksum() == c1
+    cols = np.asarray(cols)
+    want_cols = oracle.bulk_colmajor(keys, ivs, 80, T)
+    assert cols.shape == want_cols.shape and np.array_equal(cols, want_cols)
+    assert np.array_equal(rows[:, : T // 8], oracle.bulk_rowmajor(keys, ivs, 80, T)) and not rows[:, T // 8:].any()
+
+
 def test_c5_init_dominated_explicit_material(pkg, oracle, torch_cuda):
     """BASELINE config 5 shape (fresh key/IV pairs x 1 Kbit) at 2^20 pairs: explicit random
     material from host arrays, row-major output to the host, sampled rows vs the oracle."""
@@ -471,6 +494,9 @@ def test_knob_validation(pkg):
         gen.set_block_threads(48)
     with pytest.raises(ValueError):
         gen.set_chunk_clocks(64)
+    with pytest.raises((ValueError, pkg.Mk2Error)):
+        gen.set_stage_bytes(4096)
+    gen.set_stage_bytes(0)
     gen.close()
 
 
