@@ -32,6 +32,10 @@ namespace mk2 {
 // LOP3 per clock (4: 303.8, 5: 301.2, 6: 299.7) and the larger the loop body (4.9 KB per clock).
 // Defaults from the A/B on B200 (profiles/r01b_probe_rblock.txt): column-major gains up to 6;
 // row-major and init start spilling inside the block at 6 / 5.
+#ifndef MK2_DRAIN_UNROLL_HALF
+#define MK2_DRAIN_UNROLL_HALF 1
+#endif
+constexpr int DRAIN_UNROLL_HALF = MK2_DRAIN_UNROLL_HALF;  // row drain, pass 2: sector halves per iteration
 constexpr int RBLOCK_COL = MK2_RBLOCK_COL;
 constexpr int RBLOCK_ROW = MK2_RBLOCK_ROW;
 constexpr int RBLOCK_INIT = MK2_RBLOCK_INIT;
@@ -685,7 +689,7 @@ __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t 
     if (ALIGNED16 && ngrp == TG && nrows == 32) {
 #pragma unroll 1
         for (int kk = 0; kk < 8; ++kk) {
-#pragma unroll 1
+#pragma unroll DRAIN_UNROLL_HALF
             for (int half = 0; half < TG / 16; ++half) {
                 uint32_t y[4][4];  // [g4][q]
 #pragma unroll

@@ -761,6 +761,29 @@ def test_cli_gen_grain_matches_reference_cli(pkg, golden, tmp_path):
     assert cli.main(["vectors", "--algo", "grain"]) == 0
 
 
+def test_every_block_tail_length(pkg, oracle):
+    """The keystream loops run clock_block<K> (K = 6 column-major, 5 row-major) plus a one-clock tail, the init
+    kernel blocks of 4 over L_iv + 80 load clocks: every remainder of every block length, in one call and resumed."""
+    rng = np.random.default_rng(66)
+    N = 77
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    for iv_bits in (0, 1, 2, 3, 80):                                   # load clocks 80..83, 160: all remainders mod 4
+        want = oracle.bulk_colmajor(keys, ivs, iv_bits, 64)
+        with pkg.MickeyGenerator(0) as gen:
+            for T in range(1, 15):
+                gen.init_material(keys, ivs, iv_bits)
+                assert np.array_equal(gen.generate_colmajor(T), want[:T]), (iv_bits, T)
+            gen.init_material(keys, ivs, iv_bits)
+            got = np.vstack([gen.generate_colmajor(n) for n in (1, 5, 6, 7, 11, 13, 21)])   # resume at every phase
+            assert np.array_equal(got, want), iv_bits
+    want_rows = oracle.bulk_rowmajor(keys, ivs, 80, 320)
+    with pkg.MickeyGenerator(0) as gen:
+        for T in (8, 16, 24, 32, 40, 48, 248, 256, 264, 320):
+            gen.init_material(keys, ivs, 80)
+            assert np.array_equal(gen.generate_rowmajor(T), want_rows[:, : T // 8]), T
+
+
 def test_randomized_differential(pkg, oracle):
     """Seeded random sweep over instance counts, clock counts, IV lengths (uniform and ragged), layouts and
     scheduling knobs: every combination must equal the oracle bit for bit (the reference uses hypothesis for
