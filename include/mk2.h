@@ -195,6 +195,11 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
  * in flight: one being generated, one being copied out).  0 = default (32 MiB;
  * row-major tiles, which are 2-D copies, are 16x this). */
 int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes);
+/* Tuning knob: where the row-major kernel parks 256 keystream words per thread
+ * between two drains: 1 = shared memory (seven worker warps per SM fit),
+ * 2 = tensor memory (tcgen05.st / tcgen05.ld; eight fit), 0 = automatic
+ * (tensor memory).  MICKEY only: the Grain kernels always use shared memory. */
+int mk2_set_row_staging(mk2_ctx *ctx, int mode);
 int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 
 /* Diagnostics: per-job trace of the column-major persistent kernel.  Records

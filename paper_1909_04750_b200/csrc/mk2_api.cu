@@ -12,6 +12,7 @@
 
 #include "../../include/mk2.h"
 #include "mk2_kernels.cuh"
+#include "mk2_tmem.cuh"
 #include "mk2_grain.cuh"
 #include "mk2_seedgen.cuh"
 
@@ -45,6 +46,7 @@ struct mk2_ctx {
     uint32_t chunk_user = 0;             // user override of clocks per scheduling chunk (0 = automatic)
     int block_user = 0;                  // user override of threads per persistent CTA (0 = automatic)
     size_t stage_target = STAGE_BYTES;   // bytes per host-output staging tile (mk2_set_stage_bytes)
+    int row_staging = 0;                 // row-major staging tile: 0 = automatic, 1 = shared memory, 2 = tensor memory
     int last_plan_block = 0;
     uint32_t last_plan_chunk = 0;
     Trace trace = {nullptr, nullptr, 0}; // optional per-job trace (device buffers owned by the ctx)
@@ -206,6 +208,7 @@ struct Plan {
     uint32_t chunk;   // clocks per chunk
     uint32_t cpc;     // chunks per chain
     unsigned grid;
+    bool tmem;        // row-major only: staging tile in tensor memory (mk2_tmem.cuh)
 };
 
 Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
@@ -214,8 +217,10 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
     Plan p{};
     // row-major: 7 warps per SM x 1 KiB per thread = 224 KiB of the 227 KiB shared memory leave room
     // for 256-clock (full 32-byte sector) staging tiles
-    p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? (rowmajor ? 224 : 256) : 128);
-    p.tg = p.block <= 224 ? 32 : 16;  // strides: <= 128 -> 128, <= 192 -> 192, <= 224 -> 224, else (16, 256)
+    // row-major staging in tensor memory (MICKEY only): eight 256-clock tiles fit, shared memory holds seven
+    p.tmem = rowmajor && ctx->cipher == 0 && ctx->row_staging != 1;
+    p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? (rowmajor && !p.tmem ? 224 : 256) : 128);
+    p.tg = p.tmem || p.block <= 224 ? 32 : 16;  // smem strides: <= 128 -> 128, <= 192 -> 192, <= 224 -> 224, else (16, 256)
     const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::WIN : 1u);
     auto round_chunk = [&](uint64_t c) {
         c = std::max<uint64_t>(c, granule);
@@ -313,7 +318,16 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
         else if (ctx->row_lsb) MK2_GRAIN_ROW_LAUNCH(false, TGV, TSV, true);            \
         else MK2_GRAIN_ROW_LAUNCH(false, TGV, TSV, false);                             \
     } while (0)
-    if (ctx->cipher == 1) {
+    if (p.tmem) {
+        if (aligned)
+            tmem::gen_rowmajor_kernel<true><<<p.grid, p.block, 0, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
+                ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+        else
+            tmem::gen_rowmajor_kernel<false><<<p.grid, p.block, 0, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
+                ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+    } else if (ctx->cipher == 1) {
         if (ts == 128) MK2_GRAIN_ROW_PICK(32, 128);
         else if (ts == 192) MK2_GRAIN_ROW_PICK(32, 192);
         else if (ts == 224) MK2_GRAIN_ROW_PICK(32, 224);
@@ -369,7 +383,7 @@ int mk2_abi_version(void) { return 1; }
 int mk2_lop3_per_clock(void) { return 327; }
 static int rblock_of(int kernel)
 {
-    return kernel == 1 ? mk2::RBLOCK_ROW : kernel == 2 ? mk2::RBLOCK_INIT : mk2::RBLOCK_COL;
+    return kernel == 1 ? mk2::tmem::RBLOCK : kernel == 2 ? mk2::RBLOCK_INIT : mk2::RBLOCK_COL;
 }
 int mk2_rblock(int kernel) { return rblock_of(kernel); }
 int mk2_lop3_per_block(int kernel)
@@ -565,6 +579,14 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
     if (!ctx) return MK2_E_ARG;
     if (clocks != 0 && clocks < 128) return fail(ctx, MK2_E_ARG, "chunk must be 0 (auto) or at least 128 clocks");
     ctx->chunk_user = clocks;
+    return MK2_OK;
+}
+
+int mk2_set_row_staging(mk2_ctx *ctx, int mode)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (mode < 0 || mode > 2) return fail(ctx, MK2_E_ARG, "row staging mode must be 0 (automatic), 1 (shared memory) or 2 (tensor memory)");
+    ctx->row_staging = mode;
     return MK2_OK;
 }
 

@@ -85,6 +85,10 @@ class MickeyGenerator:
         """Tuning knob: clocks per scheduling chunk of the persistent keystream kernels."""
         self._ck(self._lib.mk2_set_chunk_clocks(self._ctx, int(clocks)), "mk2_set_chunk_clocks")
 
+    def set_row_staging(self, mode: int):
+        """Tuning knob: row-major staging tile in shared memory (1) or tensor memory (2); 0 = automatic."""
+        self._ck(self._lib.mk2_set_row_staging(self._ctx, int(mode)), "mk2_set_row_staging")
+
     def set_stage_bytes(self, nbytes: int):
         """Tuning knob: bytes per device staging tile when the output buffer is in host memory."""
         self._ck(self._lib.mk2_set_stage_bytes(self._ctx, int(nbytes)), "mk2_set_stage_bytes")

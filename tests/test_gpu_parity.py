@@ -736,7 +736,7 @@ def test_c3_instance_count_rowmajor_sampled(pkg, golden, oracle, torch_cuda):
         gen.generate_rowmajor(T, rows)
         torch.cuda.synchronize()
         c_row = gen.checksum()
-        assert gen.last_plan()[0] == 224                       # full-sector staging geometry
+        assert gen.last_plan()[0] == 256                       # eight worker warps: staging tiles in tensor memory
         rng = np.random.default_rng(24)
         for n in [0, 31, 32, 1023, 1024, N - 1] + rng.integers(0, N, 10).tolist():
             keys, ivs = oracle.counter_material(key, (1 << 30) + int(n), 1)
@@ -759,6 +759,35 @@ def test_cli_gen_grain_matches_reference_cli(pkg, golden, tmp_path):
         assert cli.main(["gen", "--algo", "grain", "--out", str(out), *case["argv"]]) == 0
         assert out.read_text() == case["hex"], case["argv"]
     assert cli.main(["vectors", "--algo", "grain"]) == 0
+
+
+@pytest.mark.parametrize("N,T,block,chunk", [(1000, 1408, 0, 0), (32, 8, 0, 0), (4099, 136, 64, 256), (64, 1024 + 120, 256, 512),
+                                             (32 * 32 * 20 + 5, 2048 + 264, 256, 768), (32 * 32 * 9, 512, 96, 256)])
+def test_rowmajor_tensor_memory_staging(pkg, oracle, N, T, block, chunk):
+    """mk2_set_row_staging(2): the 256-word staging tile lives in tensor memory (tcgen05.st / tcgen05.ld) instead
+    of shared memory; same bits for aligned and ragged shapes, partial last chains, every worker-warp count."""
+    rng = np.random.default_rng(N * 7 + T)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    want = oracle.bulk_rowmajor(keys, ivs, 80, T)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_row_staging(2)
+        gen.set_block_threads(block)
+        gen.set_chunk_clocks(chunk)
+        gen.init_material(keys, ivs, 80)
+        got = gen.generate_rowmajor(T)
+        c_tmem = gen.checksum()
+        half = (T // 16) * 8
+        gen.init_material(keys, ivs, 80)
+        a = np.zeros((N, T // 8 + 1), np.uint8)                       # odd pitch: the unaligned drain
+        gen.generate_rowmajor(half, a, pitch_bytes=a.shape[1])
+        gen.generate_rowmajor(T - half, a, pitch_bytes=a.shape[1], byte_offset=half // 8)
+        gen.set_row_staging(1)
+        gen.init_material(keys, ivs, 80)
+        gen.generate_rowmajor(T)
+        assert gen.checksum() == c_tmem
+    assert np.array_equal(got, want)
+    assert np.array_equal(a[:, : T // 8], want)
 
 
 def test_every_block_tail_length(pkg, oracle):

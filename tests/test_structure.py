@@ -46,7 +46,8 @@ def _innermost_clock_loops(ins, lo_lop3, hi_lop3):
     return loops
 
 
-@pytest.mark.parametrize("kernel", ["mk219gen_colmajor_kernel", "mk219gen_rowmajor_kernelILb1ELi32ELi224E"])
+@pytest.mark.parametrize("kernel", ["mk219gen_colmajor_kernel", "mk219gen_rowmajor_kernelILb1ELi32ELi224E",
+                                    "mk24tmem19gen_rowmajor_kernelILb1E"])
 def test_mickey_clock_loop_is_straight_line_lop3(kernel):
     kernels = _kernel_sass(kernel)
     assert kernels, f"{kernel} not found in libmk2.so"
@@ -67,6 +68,7 @@ def test_mickey_clock_loop_is_straight_line_lop3(kernel):
 
 @pytest.mark.parametrize("kernel,which", [("mk219gen_colmajor_kernel", 0),
                                           ("mk219gen_rowmajor_kernelILb1ELi32ELi224E", 1),
+                                          ("mk24tmem19gen_rowmajor_kernelILb1E", 1),
                                           ("mk211init_kernelILb0E", 2)])
 def test_blocked_clock_loop_matches_the_predicted_lop3_count(kernel, which):
     lib = _native.lib()
@@ -88,6 +90,19 @@ def test_blocked_clock_loop_matches_the_predicted_lop3_count(kernel, which):
                 assert not [t for t in texts if re.search(r"\b(LDL|STL)\b", t)]
             alu = [t for t in texts if re.match(r"(LOP3|IADD3|SHF|PRMT|LEA|ISETP|SEL|VIADD|IABS|VIMNMX)", t)]
             assert len(alu) <= n + 3 * K, (len(alu), n)                 # pointer / checksum adds only
+
+
+def test_tensor_memory_kernel_uses_tcgen05_and_no_shared_memory_tile():
+    """The default row-major kernel stages keystream in tensor memory: STTM / LDTM in the SASS, the allocation
+    (UTCATOMSWS) at entry, and no shared-memory loads or stores in its loops."""
+    (name, ins), = _kernel_sass("mk24tmem19gen_rowmajor_kernelILb1E").items()
+    texts = [t for _, t in ins]
+    assert sum(t.startswith("STTM") for t in texts) >= 6 and sum(t.startswith("LDTM") for t in texts) >= 17
+    assert any("UTCATOMSWS" in t for t in texts)
+    # shared memory carries only the allocation's address slot (prologue / epilogue), never keystream
+    assert len([t for t in texts if re.match(r"(@!?U?P\d+\s+)?(LDS|STS)\b", t)]) <= 8
+    for body in _innermost_clock_loops(ins, 20, 4000):
+        assert not [t for _, t in body if re.match(r"(@!?U?P\d+\s+)?(LDS|STS)\b", t)]
 
 
 def test_init_and_grain_loops_have_no_spills_or_branches():
