@@ -36,7 +36,7 @@ LOP3_PER_CLOCK_SURVEY = 327  # LOP3 per clock per 32-lane word, 
 # `ncu --set full` captures (per launch, like roofline.achieved); only for launches captured exactly.
 NCU_TRAFFIC = {
     # (layout, instances, clocks): (bytes, source)
-    ("colmajor", 1 << 20, 1_000_000): (131_457_221_000 + 503_661_568, "profiles/r01_ncu_gen_colmajor_c2_full_1Mclk.txt"),
+    ("colmajor", 1 << 20, 1_000_000): (131_438_553_000 + 512_053_248, "profiles/r01b_ncu_gen_colmajor_c2_full_1Mclk.txt"),
 }
 
 
