@@ -186,6 +186,21 @@ int mk2_last_kernel_launches(const mk2_ctx *ctx);
  * themselves); mk2_last_kernel_ms is then only valid after mk2_sync. */
 int mk2_set_async(mk2_ctx *ctx, int async);
 
+/*
+ * One-shot bulk generation, row-major: key/IV load + pre-clocks + T keystream bits
+ * of N instances in one call -- kernels.mickey_sliced_words (kernels.py:189-200)
+ * followed by words_lane_major_bytes (kernels.py:615-621) in the reference, for
+ * any N.  Arguments as mk2_init_from_material / mk2_generate_rowmajor; keys and
+ * ivs must both be host or both be device pointers.  With host buffers the
+ * instances are processed in blocks (2 x 8 x SMs x 1024) and the upload of block
+ * b+1, the init + keystream of block b and the download of block b-1 overlap on
+ * three streams.  *checksum (optional) receives what mk2_checksum would return for
+ * the whole call.  When N spans more than one block the context holds no
+ * resumable state afterwards (mk2_init_* again before mk2_generate_*).
+ */
+int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride, uint32_t iv_bits,
+                      uint64_t N, uint64_t T, void *out, uint64_t pitch_bytes, uint64_t *checksum);
+
 /* Tuning knob: clocks per scheduling chunk of the persistent keystream kernels
  * (0 = automatic, else >= 128): a chain of 1024 instances runs one chunk, parks
  * its state and goes back to the ready queue.

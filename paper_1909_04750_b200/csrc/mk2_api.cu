@@ -31,7 +31,10 @@ constexpr size_t ROW_TILE_FACTOR = 16;
 struct mk2_ctx {
     int device = 0;
     int sm_count = 0;
-    cudaStream_t own = nullptr, stream = nullptr, copy = nullptr;
+    cudaStream_t own = nullptr, stream = nullptr, copy = nullptr, h2d = nullptr;  // h2d: mk2_bulk_rowmajor only (lazy)
+    cudaEvent_t h2d_done[2] = {nullptr, nullptr}, mat_used[2] = {nullptr, nullptr};
+    void *d_bulk_in[2] = {nullptr, nullptr};  // material staging of mk2_bulk_rowmajor
+    size_t bulk_in_bytes = 0;
     cudaMemPool_t pool = nullptr;  // private stream-ordered pool for scratch (kept warm: no trim at sync points)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t gen_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
@@ -486,7 +489,11 @@ int mk2_destroy(mk2_ctx *ctx)
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->copy) cudaStreamSynchronize(ctx->copy);
+    if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
     for (int b = 0; b < 2; ++b) {
+        if (ctx->d_bulk_in[b]) cudaFree(ctx->d_bulk_in[b]);
+        if (ctx->h2d_done[b]) cudaEventDestroy(ctx->h2d_done[b]);
+        if (ctx->mat_used[b]) cudaEventDestroy(ctx->mat_used[b]);
         if (ctx->d_stage[b]) cudaFree(ctx->d_stage[b]);
         if (ctx->gen_done[b]) cudaEventDestroy(ctx->gen_done[b]);
         if (ctx->copy_done[b]) cudaEventDestroy(ctx->copy_done[b]);
@@ -504,6 +511,7 @@ int mk2_destroy(mk2_ctx *ctx)
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     delete ctx;
     return MK2_OK;
 }
@@ -681,6 +689,21 @@ static int init_common(mk2_ctx *ctx, uint64_t N)
     return MK2_OK;
 }
 
+// pack + key/IV load + pre-clock of the ctx->N instances whose material is on the device
+static int init_uniform_device(mk2_ctx *ctx, const uint8_t *dk, const uint8_t *di, uint32_t iv_stride, uint32_t iv_bits)
+{
+    int rc;
+    uint32_t *mat = nullptr;
+    const int load = (int)iv_bits + KEY_BITS;
+    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->pool, ctx->stream));
+    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, ctx->N, ctx->G, mat);
+    CK(cudaGetLastError());
+    ctx->last_launches++;
+    if ((rc = launch_init(ctx, mat, load, 0, false))) return rc;
+    CK(cudaFreeAsync(mat, ctx->stream));
+    return MK2_OK;
+}
+
 int mk2_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
                            uint32_t iv_bits, uint64_t N)
 {
@@ -692,16 +715,9 @@ int mk2_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs
     if ((rc = begin_timing(ctx))) return rc;
     const uint8_t *dk = nullptr, *di = nullptr;
     void *ok = nullptr, *oi = nullptr;
-    uint32_t *mat = nullptr;
     if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
     if ((rc = stage_input(ctx, iv_bits ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
-    const int load = (int)iv_bits + KEY_BITS;
-    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->pool, ctx->stream));
-    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, N, ctx->G, mat);
-    CK(cudaGetLastError());
-    ctx->last_launches++;
-    if ((rc = launch_init(ctx, mat, load, 0, false))) return rc;
-    CK(cudaFreeAsync(mat, ctx->stream));
+    if ((rc = init_uniform_device(ctx, dk, di, iv_stride, iv_bits))) return rc;
     if (ok) CK(cudaFreeAsync(ok, ctx->stream));
     if (oi) CK(cudaFreeAsync(oi, ctx->stream));
     return end_timing(ctx);
@@ -946,6 +962,51 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
     return end_timing(ctx);
 }
 
+// Host row-major output of every chain of the context: 2-D tiles [block of chains] x [time chunk]
+// through two device staging buffers (`b` = which one comes next; copies are left in flight:
+// drain_copies).  A tile is a contiguous run of instance rows, each >= 512 B wide whenever T allows,
+// so the D2H copy is one wide 2-D (or plain 1-D) transfer; a chain block is large enough to occupy
+// every worker warp.  Chains stay strictly serial in time because the time loop is the inner one.
+static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch_bytes, int &b)
+{
+    int rc;
+    const uint64_t chains = (ctx->G + 31) / 32;
+    // tile = [block_chains x 1024 rows] x [tc_max clocks] of about ROW_TILE_FACTOR x stage_target bytes, rows at
+    // least 512 B wide when T allows (narrower 2-D copies collapse: 192 B rows 37 GB/s, 64 B rows 16 GB/s), and
+    // between one and two chains per worker warp of a full launch
+    const uint64_t tile_bytes = ROW_TILE_FACTOR * ctx->stage_target;
+    const uint64_t min_clocks = std::min<uint64_t>((T + 255) / 256 * 256, 4096);
+    const uint64_t workers = 8ull * (uint64_t)ctx->sm_count;
+    const uint64_t want_chains = std::min<uint64_t>(2 * workers, std::max<uint64_t>(workers, tile_bytes / (min_clocks / 8) / 1024));
+    const uint64_t block_chains = std::min<uint64_t>(chains, want_chains);
+    const uint64_t block_rows = block_chains * 1024;
+    uint64_t tc_max = std::max<uint64_t>(min_clocks, tile_bytes / block_rows / 32 * 256);
+    tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
+    if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
+    for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {
+        const uint64_t nch = std::min(block_chains, chains - c0);
+        const uint64_t row0 = c0 * 1024;
+        const uint64_t nrows = std::min<uint64_t>(nch * 1024, ctx->N - row0);
+        for (uint64_t t0 = 0; t0 < T; t0 += tc_max, b ^= 1) {
+            const uint64_t tc = std::min(tc_max, T - t0);
+            const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
+            if ((rc = acquire_stage(ctx, b))) return rc;
+            if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp, c0, nch))) return rc;
+            CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
+            uint8_t *dst = out + row0 * pitch_bytes + t0 / 8;
+            if (sp == tc / 8 && pitch_bytes == sp)
+                CK(cudaMemcpyAsync(dst, ctx->d_stage[b], nrows * sp, cudaMemcpyDeviceToHost, ctx->copy));
+            else
+                CK(cudaMemcpy2DAsync(dst, pitch_bytes, ctx->d_stage[b], sp, tc / 8, nrows, cudaMemcpyDeviceToHost,
+                                     ctx->copy));
+            CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
+            ctx->copy_pending[b] = true;
+        }
+    }
+    return MK2_OK;
+}
+
 static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes)
 {
     int rc = check_ready(ctx);
@@ -963,42 +1024,119 @@ static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
     if (is_device_ptr(out)) {
         if ((rc = launch_row(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, 0, chains))) return rc;
     } else {
-        // Host output: 2-D tiles [block of chains] x [time chunk] through two device staging
-        // buffers.  A tile is a contiguous run of instance rows, each >= 512 B wide whenever T
-        // allows, so the D2H copy is one wide 2-D (or plain 1-D) transfer; a chain block is
-        // large enough to occupy every worker warp.  Chains stay strictly serial in time
-        // because the time loop is the inner one.
-        const uint64_t block_chains = std::min<uint64_t>(chains, 2ull * 8ull * (uint64_t)ctx->sm_count);
-        const uint64_t block_rows = block_chains * 1024;
-        uint64_t tc_max = std::max<uint64_t>(256, ROW_TILE_FACTOR * ctx->stage_target / block_rows / 32 * 256);
-        tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
-        if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
         int b = 0;
-        for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {
-            const uint64_t nch = std::min(block_chains, chains - c0);
-            const uint64_t row0 = c0 * 1024;
-            const uint64_t nrows = std::min<uint64_t>(nch * 1024, ctx->N - row0);
-            for (uint64_t t0 = 0; t0 < T; t0 += tc_max, b ^= 1) {
-                const uint64_t tc = std::min(tc_max, T - t0);
-                const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
-                if ((rc = acquire_stage(ctx, b))) return rc;
-                if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp, c0, nch))) return rc;
-                CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
-                CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
-                uint8_t *dst = static_cast<uint8_t *>(out) + row0 * pitch_bytes + t0 / 8;
-                if (sp == tc / 8 && pitch_bytes == sp)
-                    CK(cudaMemcpyAsync(dst, ctx->d_stage[b], nrows * sp, cudaMemcpyDeviceToHost, ctx->copy));
-                else
-                    CK(cudaMemcpy2DAsync(dst, pitch_bytes, ctx->d_stage[b], sp, tc / 8, nrows, cudaMemcpyDeviceToHost,
-                                         ctx->copy));
-                CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
-                ctx->copy_pending[b] = true;
-            }
-        }
+        if ((rc = rowmajor_to_host(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, b))) return rc;
         if ((rc = drain_copies(ctx))) return rc;
     }
     ctx->clocks += T;
     return end_timing(ctx);
+}
+
+// ---------------------------------------------------------------------------
+// One-shot bulk generation, row-major: init + keystream of N instances x T bits
+// in one call (what kernels.mickey_sliced_words + words_lane_major_bytes do in the
+// reference, kernels.py:189-200 / :615-621).  With host buffers the instances are
+// processed in blocks and the three stages of consecutive blocks overlap:
+//     H2D of block b+1's key/IV bytes | pack + init + keystream of block b | D2H of block b-1
+// on three streams, so the upload and the init hide behind the (link-bound) download.
+// The context keeps no resumable state afterwards.
+// ---------------------------------------------------------------------------
+int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride, uint32_t iv_bits,
+                      uint64_t N, uint64_t T, void *out, uint64_t pitch_bytes, uint64_t *checksum)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MK2_E_CUDA, "cudaSetDevice failed");
+    if (!keys) return fail(ctx, MK2_E_ARG, "keys is NULL");
+    if (N == 0) return fail(ctx, MK2_E_ARG, "at least one instance is required");
+    if (iv_bits > 80) return fail(ctx, MK2_E_ARG, "IV must be at most 80 bits");
+    if (iv_bits && (!ivs || iv_stride < (iv_bits + 7) / 8)) return fail(ctx, MK2_E_ARG, "ivs/iv_stride too small for iv_bits");
+    if (T == 0 || T % 8) return fail(ctx, MK2_E_ARG, "bit count must be a positive multiple of 8");
+    if (!out) return fail(ctx, MK2_E_ARG, "out is NULL");
+    if (pitch_bytes < T / 8) return fail(ctx, MK2_E_ARG, "pitch_bytes smaller than T/8");
+    int rc;
+    const bool in_dev = is_device_ptr(keys), out_dev = is_device_ptr(out);
+    if (iv_bits && is_device_ptr(ivs) != in_dev) return fail(ctx, MK2_E_ARG, "keys and ivs must both be host or both be device pointers");
+    const uint64_t block_inst = 2ull * 8ull * (uint64_t)ctx->sm_count * 1024ull;  // two chains per worker warp
+    if (!ctx->h2d) {
+        CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&ctx->h2d_done[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->mat_used[i], cudaEventDisableTiming));
+        }
+    }
+    const size_t in_row = 10 + (iv_bits ? (size_t)iv_stride : 0);
+    const size_t in_bytes = (size_t)std::min<uint64_t>(N, block_inst) * in_row;
+    if (!in_dev && in_bytes > ctx->bulk_in_bytes) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaStreamSynchronize(ctx->h2d));
+        for (int i = 0; i < 2; ++i) {
+            if (ctx->d_bulk_in[i]) cudaFree(ctx->d_bulk_in[i]);
+            ctx->d_bulk_in[i] = nullptr;
+        }
+        ctx->bulk_in_bytes = 0;
+        for (int i = 0; i < 2; ++i) CK(cudaMalloc(&ctx->d_bulk_in[i], in_bytes));
+        ctx->bulk_in_bytes = in_bytes;
+    }
+    if ((rc = init_common(ctx, std::min<uint64_t>(N, block_inst)))) return rc;
+    ctx->last_launches = 0;
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_sum, 0, sizeof(unsigned long long), ctx->stream));
+    CK(cudaEventRecord(ctx->mat_used[0], ctx->stream));  // everything queued before this call is ahead of the uploads
+    CK(cudaStreamWaitEvent(ctx->h2d, ctx->mat_used[0], 0));
+    int sb = 0, launches = 0;
+    uint64_t nblk = 0;
+    for (uint64_t row0 = 0; row0 < N; row0 += block_inst, ++nblk) {
+        const uint64_t n = std::min(block_inst, N - row0);
+        const int i = (int)(nblk & 1);
+        const uint8_t *dk, *di = nullptr;
+        if (in_dev) {
+            dk = keys + row0 * 10;
+            if (iv_bits) di = ivs + row0 * (uint64_t)iv_stride;
+        } else {
+            uint8_t *buf = static_cast<uint8_t *>(ctx->d_bulk_in[i]);
+            if (nblk >= 2) CK(cudaStreamWaitEvent(ctx->h2d, ctx->mat_used[i], 0));  // block b-2 has been packed
+            CK(cudaMemcpyAsync(buf, keys + row0 * 10, n * 10, cudaMemcpyHostToDevice, ctx->h2d));
+            if (iv_bits)
+                CK(cudaMemcpyAsync(buf + n * 10, ivs + row0 * (uint64_t)iv_stride, n * (size_t)iv_stride,
+                                   cudaMemcpyHostToDevice, ctx->h2d));
+            CK(cudaEventRecord(ctx->h2d_done[i], ctx->h2d));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->h2d_done[i], 0));
+            dk = buf;
+            if (iv_bits) di = buf + n * 10;
+        }
+        ctx->N = n;
+        ctx->G = (n + 31) / 32;
+        if ((rc = init_uniform_device(ctx, dk, di, iv_stride, iv_bits))) return rc;
+        if (!in_dev) CK(cudaEventRecord(ctx->mat_used[i], ctx->stream));
+        uint8_t *dst = static_cast<uint8_t *>(out) + row0 * pitch_bytes;
+        if (out_dev) {
+            if ((rc = launch_row(ctx, T, dst, pitch_bytes, 0, (ctx->G + 31) / 32))) return rc;
+        } else {
+            if ((rc = rowmajor_to_host(ctx, T, dst, pitch_bytes, sb))) return rc;
+        }
+        // checksum of the whole call: block sums accumulate in d_sum (block starts are multiples of 64 instances,
+        // so the parity term of checksum_kernel is that of the global group index)
+        const unsigned nb = std::min<unsigned>(blocks_for(ctx->G), 4u * (unsigned)ctx->sm_count);
+        checksum_kernel<<<nb, BLOCK, 0, ctx->stream>>>(ctx->d_acc, ctx->G, ctx->g_offset + row0 / 32, ctx->d_sum);
+        CK(cudaGetLastError());
+        launches += ctx->last_launches + 1;
+    }
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, ctx->d_sum, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!out_dev && (rc = drain_copies(ctx))) return rc;
+    CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+    ctx->timing_open = false;
+    ctx->last_launches = launches;
+    if (checksum) *checksum = v;
+    if (nblk > 1) {  // only the last block's state is on the device: nothing to resume from
+        ctx->ready = false;
+        ctx->N = ctx->G = 0;
+    } else {
+        ctx->clocks = T;
+    }
+    return MK2_OK;
 }
 
 int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n)

@@ -580,8 +580,9 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
 #pragma unroll 1
             while (t < tc) {
                 const uint32_t nseg = tc - t < seg_max ? (uint32_t)(tc - t) : seg_max;
-                uint32_t idx = 0, u = 0;
-                uint32_t *p = base;
+                [[maybe_unused]] uint32_t idx = 0;
+                [[maybe_unused]] uint32_t *p = base;
+                uint32_t u = 0;
                 HalfSums hs;
                 auto emit = [&](uint32_t z) {
 #if MK2_COL_ADDR

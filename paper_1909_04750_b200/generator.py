@@ -222,6 +222,25 @@ class MickeyGenerator:
                  "mk2_generate_rowmajor")
         return out
 
+    def bulk_rowmajor(self, keys, ivs, iv_bits: int, nclocks: int, out=None, pitch_bytes: Optional[int] = None):
+        """One shot: init from (keys, ivs) + nclocks keystream bits per instance, row-major (the reference's
+        mickey_sliced_words + words_lane_major_bytes for any N).  With host arrays the upload, the init +
+        keystream and the download of consecutive instance blocks overlap.  Returns (out, checksum)."""
+        if nclocks % 8:
+            raise ValueError("bit count must be a multiple of 8")
+        n, iv_stride = _material_shape(keys, ivs, iv_bits)
+        if out is None:
+            pitch = nclocks // 8 if pitch_bytes is None else int(pitch_bytes)
+            out = np.empty((n, pitch), np.uint8)
+        elif pitch_bytes is None:
+            pitch = int(out.shape[-1]) * (out.element_size() if _is_torch(out) else out.itemsize)
+        else:
+            pitch = int(pitch_bytes)
+        csum = C.c_uint64(0)
+        self._ck(self._lib.mk2_bulk_rowmajor(self._ctx, _ptr(keys), _ptr(ivs) if iv_bits else 0, iv_stride, int(iv_bits),
+                                             n, int(nclocks), _ptr(out), pitch, C.byref(csum)), "mk2_bulk_rowmajor")
+        return out, int(csum.value)
+
     def clock(self, mixing: bool, input_words=None, n: int = 1):
         """n raw CLOCK_KG steps (no output); input_words uint32[n][G] or None."""
         self._ck(self._lib.mk2_clock(self._ctx, int(bool(mixing)), _ptr(input_words), int(n)), "mk2_clock")

@@ -41,8 +41,13 @@ def bulk_colmajor(keys, ivs, iv_bits, nclocks: int, device: int = 0, out=None):
 
 
 def bulk_rowmajor(keys, ivs, iv_bits, nclocks: int, device: int = 0, out=None):
-    """N instances -> uint8 out[N][nclocks/8], MSB-first rows (lane-major order)."""
+    """N instances -> uint8 out[N][nclocks/8], MSB-first rows (lane-major order).
+
+    Uniform IV length: one mk2_bulk_rowmajor call (upload, init + keystream and download of consecutive
+    instance blocks overlap); ragged IV lengths: init, then generate."""
     with MickeyGenerator(device) as gen:
+        if np.isscalar(iv_bits) and nclocks > 0:
+            return gen.bulk_rowmajor(keys, ivs, int(iv_bits), nclocks, out)[0]
         _init(gen, keys, ivs, iv_bits)
         return gen.generate_rowmajor(nclocks, out)
 

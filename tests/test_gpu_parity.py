@@ -393,7 +393,8 @@ def test_rowmajor_host_output_tiles(pkg, oracle):
         assert gen.checksum() == csum
     assert not rows[:, T // 8:].any()
     rng = np.random.default_rng(5)
-    idx = np.unique(np.concatenate([[0, 1023, 1024, 2368 * 1024 - 1, 2368 * 1024, N - 1], rng.integers(0, N, 60)]))
+    idx = np.unique(np.concatenate([[0, 1023, 1024, 1184 * 1024 - 1, 1184 * 1024, 2368 * 1024 - 1, 2368 * 1024, N - 1],
+                                    rng.integers(0, N, 60)]))
     for n in idx:
         keys, ivs = oracle.counter_material(key, int(n), 1)
         assert rows[n, : T // 8].tobytes() == oracle.bulk_rowmajor(keys, ivs, 80, T)[0].tobytes(), n
@@ -788,6 +789,41 @@ def test_rowmajor_tensor_memory_staging(pkg, oracle, N, T, block, chunk):
         assert gen.checksum() == c_tmem
     assert np.array_equal(got, want)
     assert np.array_equal(a[:, : T // 8], want)
+
+
+def test_bulk_rowmajor_one_shot_pipelined_blocks(pkg, oracle, torch_cuda):
+    """mk2_bulk_rowmajor: N spans three pipeline blocks (2 x 8 x SMs x 1024 instances each); host and device
+    buffers, IV lengths 80 / 13 / 0; rows and the whole-call checksum equal init + generate and the oracle."""
+    torch = torch_cuda
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    block = 2 * 8 * sms * 1024
+    N, T = 2 * block + 32 * 1000 + 9, 256
+    rng = np.random.default_rng(99)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    sample = np.unique(np.concatenate([[0, block - 1, block, 2 * block - 1, 2 * block, N - 1], rng.integers(0, N, 40)]))
+    with pkg.MickeyGenerator(0) as gen:
+        for iv_bits in (80, 13, 0):
+            rows, csum = gen.bulk_rowmajor(keys, ivs, iv_bits, T)
+            want = oracle.bulk_rowmajor(keys[sample], ivs[sample], iv_bits, T)
+            assert np.array_equal(rows[sample], want), iv_bits
+            gen.init_material(keys, ivs if iv_bits else None, iv_bits)
+            ref_rows = gen.generate_rowmajor(T)
+            assert gen.checksum() == csum and np.array_equal(rows, ref_rows), iv_bits
+            gen.bulk_rowmajor(keys, ivs, iv_bits, 8)
+            with pytest.raises(pkg.Mk2Error):                   # a multi-block bulk call leaves no resumable state
+                gen.generate_rowmajor(8)
+        # device buffers in, device buffer out, pitch wider than the row
+        dk, di = torch.from_numpy(keys).cuda(), torch.from_numpy(ivs).cuda()
+        dout = torch.zeros((N, T // 8 + 16), dtype=torch.uint8, device="cuda")
+        _, csum_dev = gen.bulk_rowmajor(dk, di, 80, T, dout)
+        rows80, csum80 = gen.bulk_rowmajor(keys, ivs, 80, T)
+        assert csum_dev == csum80 and np.array_equal(dout[:, : T // 8].cpu().numpy(), rows80)
+        # one block only: the context stays resumable
+        small, _ = gen.bulk_rowmajor(keys[:5000], ivs[:5000], 80, 64)
+        more = gen.generate_rowmajor(64)
+        both = oracle.bulk_rowmajor(keys[:5000], ivs[:5000], 80, 128)
+        assert np.array_equal(np.hstack([small, more]), both)
 
 
 def test_every_block_tail_length(pkg, oracle):
