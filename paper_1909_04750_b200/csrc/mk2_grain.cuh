@@ -216,6 +216,47 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             uint32_t b[GW], s[GW];
             unsigned long long a;
             load_state(state, acc, G, g, b, s, a);
+#ifndef MK2_GRAIN_COL_FMA
+#define MK2_GRAIN_COL_FMA 1
+#endif
+#if MK2_GRAIN_COL_FMA
+            // Output addressing and checksum off the ALU pipe (a 64-bit pointer bump and a 64-bit accumulate are
+            // 3 of 40 ALU-pipe instructions per clock here): 64-bit base + 32-bit element index (IMAD.WIDE, the
+            // index lives on the uniform datapath) and IDP.2A half sums; segments of < 2^32 elements, <= 65536 words.
+            uint32_t *base = out + t0 * stride + g;
+            const uint32_t stride32 = (uint32_t)stride;  // host side guarantees stride < 2^30
+            uint32_t seg_max = 0xFFFFFFFFu / stride32;
+            if (seg_max > HALFSUM_MAX_WORDS) seg_max = HALFSUM_MAX_WORDS;
+            if (seg_max > WIN) seg_max -= seg_max % WIN;
+            uint64_t t = 0;
+#pragma unroll 1
+            while (t < tc) {
+                const uint32_t nseg = tc - t < seg_max ? (uint32_t)(tc - t) : seg_max;
+                uint32_t idx = 0, u = 0;
+                HalfSums hs;
+#pragma unroll 1
+                for (; u + WIN <= nseg; u += WIN) {
+                    static_for_up<0, WIN>([&](auto ic) {
+                        const uint32_t z = step<decltype(ic)::value, false>(b, s);
+                        base[idx] = z;
+                        idx += stride32;
+                        hs.add(z);
+                    });
+                    realign<WIN>(b, s);
+                }
+#pragma unroll 1
+                for (; u < nseg; ++u) {
+                    const uint32_t z = step<0, false>(b, s);
+                    base[idx] = z;
+                    idx += stride32;
+                    hs.add(z);
+                    realign<1>(b, s);
+                }
+                hs.fold(a);
+                base += (uint64_t)nseg * stride;
+                t += nseg;
+            }
+#else
             uint32_t *p = out + t0 * stride + g;
             uint64_t t = 0;
 #pragma unroll 1
@@ -236,6 +277,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 acc_add(a, z);
                 realign<1>(b, s);
             }
+#endif
             store_state(state_out, acc_out, G, g, b, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
@@ -269,13 +311,14 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);  // a multiple of 8
                 uint32_t *zp = col;
                 int t = 0;
+                HalfSums hs;  // checksum on the FMA pipe; a tile is at most 256 words
 #pragma unroll 1
                 for (; t + WIN <= nclk; t += WIN) {
                     static_for_up<0, WIN>([&](auto ic) {
                         constexpr int c = decltype(ic)::value;
                         const uint32_t z = step<c, false>(b, s);
                         zp[c * ts] = z;
-                        acc_add(a, z);
+                        hs.add(z);
                     });
                     zp += WIN * ts;
                     realign<WIN>(b, s);
@@ -285,9 +328,10 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     const uint32_t z = step<0, false>(b, s);
                     *zp = z;
                     zp += ts;
-                    acc_add(a, z);
+                    hs.add(z);
                     realign<1>(b, s);
                 }
+                hs.fold(a);
                 row_drain<ALIGNED16, TG, TS, LSB>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
             }
             store_state(state_out, acc_out, G, g, b, s, a);

@@ -14,7 +14,7 @@ import torch
 import paper_1909_04750_b200 as pkg
 from paper_1909_04750_b200 import grain
 
-GRAIN_ALU_PER_CLOCK = 40.5  # SASS: 598 LOP3 + 50 other ALU-pipe instructions per 16 clocks (profiles/r01_sass_loop_stats.txt)
+GRAIN_ALU_PER_CLOCK = 37.4  # SASS: 598 LOP3 and nothing else on the ALU pipe per 16 clocks (profiles/r01b_sass_loop_stats.txt)
 
 
 def best_ms(fn, gen, warm=3, reps=5):
