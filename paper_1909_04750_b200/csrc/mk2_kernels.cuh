@@ -32,6 +32,17 @@ namespace mk2 {
 // LOP3 per clock (4: 303.8, 5: 301.2, 6: 299.7) and the larger the loop body (4.9 KB per clock).
 // Defaults from the A/B on B200 (profiles/r01b_probe_rblock.txt): column-major gains up to 6;
 // row-major and init start spilling inside the block at 6 / 5.
+// Column-major loop: output addressing (0 = 64-bit pointer bump, 1 = 32-bit index) and checksum (0 = mad.wide
+// accumulate, 1 = IDP.2A half sums); row-major loop: checksum likewise.  See gen_colmajor_kernel.
+#ifndef MK2_COL_ADDR
+#define MK2_COL_ADDR 0
+#endif
+#ifndef MK2_COL_SUM
+#define MK2_COL_SUM 0
+#endif
+#ifndef MK2_ROW_SUM
+#define MK2_ROW_SUM 1
+#endif
 #ifndef MK2_DRAIN_UNROLL_HALF
 #define MK2_DRAIN_UNROLL_HALF 1
 #endif
@@ -558,12 +569,6 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             uint32_t r[NBITS], s[NBITS];
             unsigned long long a;
             load_state(state, acc, G, g, r, s, a);
-#ifndef MK2_COL_ADDR
-#define MK2_COL_ADDR 0
-#endif
-#ifndef MK2_COL_SUM
-#define MK2_COL_SUM 0
-#endif
             // Build-time experiment knobs (profiles/r01b_probe_col_row_variants.txt).  MK2_COL_ADDR 1: a
             // 64-bit base and a 32-bit element index (index * 4 + base is one IMAD.WIDE, the index bump a
             // uniform-datapath IMAD) instead of a 64-bit pointer bump (IADD3 + IMAD.X per clock);
@@ -624,17 +629,19 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
 // Keystream, row-major: out[(32 g + j) * pitch + t / 8], MSB-first bytes
 // (kernels.py:604-621, bitops.py:20-23).
 //
-// The clock loop is the same one-clock body as above, except that z_t goes to
-// the thread's private shared-memory column (tile[t % 128][tid], conflict-free)
-// instead of HBM: the 200 state words leave no registers to hold keystream.
-// Every 128 clocks the thread drains its column in two small loops:
+// The clock loop is the blocked loop of the column-major kernel, except that z_t goes to
+// a per-thread staging tile instead of HBM: the 200 state words leave no registers to
+// hold keystream.  This kernel keeps the tile in a private shared-memory column
+// (tile[t][tid], conflict-free); the default for MICKEY, tmem::gen_rowmajor_kernel in
+// mk2_tmem.cuh, keeps it in tensor memory with the same two-pass drain.  Every 8 * TG
+// clocks (256 = a full 32-byte sector per instance row) the thread drains its tile:
 //   pass 1  per 8 clocks: 8 words back into registers, 8x32 bit transpose
-//           (word k, byte q = the output byte of instance 8q + k), back to smem;
+//           (word k, byte q = the output byte of instance 8q + k), back in place;
 //   pass 2  per k: 16 words (one per 8-clock group) -> 4x4 byte transposes with
-//           PRMT -> one 16-byte store per instance row.
-// Each thread only ever reads what it wrote, so no barrier is needed; the code
-// stays small enough for the instruction cache (an 8-clock unrolled body is
-// 43 KB and measurably starves instruction fetch).
+//           PRMT -> one 16-byte store per instance row, the two halves of a sector
+//           back to back.
+// Each thread only ever reads what it wrote, so no barrier is needed; the drain loops
+// are not unrolled further, which keeps the code inside the instruction cache.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
 {
@@ -749,9 +756,6 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             for (uint64_t t0 = 0; t0 < tc; t0 += 8 * TG) {
                 const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);
                 const int ngrp = nclk >> 3;
-#ifndef MK2_ROW_SUM
-#define MK2_ROW_SUM 1
-#endif
                 uint32_t *zp = col;
                 int t = 0;
                 HalfSums hs;  // a tile is at most 256 words
