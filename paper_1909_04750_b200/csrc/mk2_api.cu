@@ -931,6 +931,7 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
     }
     if (!out) return fail(ctx, MK2_E_ARG, "out is NULL");
     if (stride_words < ctx->G) return fail(ctx, MK2_E_ARG, "stride_words smaller than the group count");
+    if (stride_words >= (1ull << 30)) return fail(ctx, MK2_E_ARG, "stride_words must be below 2^30");  // 32-bit byte strides in the kernels
     if (reinterpret_cast<uintptr_t>(out) % 4) return fail(ctx, MK2_E_ARG, "out must be 4-byte aligned");
     if ((rc = begin_timing(ctx))) return rc;
     if (is_device_ptr(out)) {

@@ -46,6 +46,10 @@ namespace mk2 {
 #ifndef MK2_DRAIN_UNROLL_HALF
 #define MK2_DRAIN_UNROLL_HALF 1
 #endif
+#ifndef MK2_COL_LOOP_UNROLL
+#define MK2_COL_LOOP_UNROLL 1
+#endif
+constexpr int COL_LOOP_UNROLL = MK2_COL_LOOP_UNROLL;  // clock_blocks per iteration of the column-major loop
 constexpr int DRAIN_UNROLL_HALF = MK2_DRAIN_UNROLL_HALF;  // row drain, pass 2: sector halves per iteration
 constexpr int RBLOCK_COL = MK2_RBLOCK_COL;
 constexpr int RBLOCK_ROW = MK2_RBLOCK_ROW;
@@ -353,6 +357,7 @@ struct HalfSums {
     }
 };
 constexpr uint32_t HALFSUM_MAX_WORDS = 65536;
+static_assert((unsigned long long)HALFSUM_MAX_WORDS * 0xFFFFull <= 0xFFFFFFFFull, "half sums must fit 32 bits");
 // pointer += bytes: as a mad.wide ptxas puts the carry half on the FMA pipe (IADD3 + IMAD.X)
 template <class P>
 __device__ __forceinline__ void ptr_add(P *&p, uint32_t bytes)
@@ -604,7 +609,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
 #endif
                 };
                 if constexpr (RBLOCK_COL > 1) {
-#pragma unroll 1
+#pragma unroll COL_LOOP_UNROLL
                     for (; u + RBLOCK_COL <= nseg; u += RBLOCK_COL)
                         clock_block<RBLOCK_COL, false, false, true>(r, s, NoInput{}, [&](auto, uint32_t z) { emit(z); });
                 }
