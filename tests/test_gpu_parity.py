@@ -379,6 +379,108 @@ def test_c2_instance_count_sampled_and_checksummed(pkg, golden, oracle, torch_cu
         gen.set_stream(None)
 
 
+def _free_gib(torch):
+    torch.cuda.empty_cache()
+    return torch.cuda.mem_get_info()[0] / 2**30
+
+
+def test_c2_full_size_million_bits(pkg, golden, oracle, torch_cuda):
+    """BASELINE config 2 at its FULL size -- 2^20 instances x 10^6 bits, 131 GB of column-major keystream resident
+    in HBM: the in-kernel checksum equals the sum of the emitted buffer, two half-length calls resume to the same
+    checksum (chunked = unchunked), and sampled 64-instance groups are bit-exact against the oracle over the
+    whole 1 Mbit."""
+    torch = torch_cuda
+    N, T = 1 << 20, 1_000_000
+    G = N // 32
+    if _free_gib(torch) < T * G * 4 / 2**30 + 6:
+        pytest.skip("needs 131 GB of free HBM")
+    key = bytes.fromhex(golden["kats"][0]["key"])
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stream(torch.cuda.current_stream().cuda_stream)
+        gen.init_counter(key, 0, N)
+        col = torch.empty((T, G), dtype=torch.int32, device="cuda")
+        gen.generate_colmajor(T, col)
+        torch.cuda.synchronize()
+        csum = gen.checksum()
+        total = 0
+        for part in col.view(torch.int64).split(1 << 14):        # exact mod 2^64: int64 sums wrap
+            total = (total + int(part.sum().item())) % (1 << 64)
+        assert total == csum
+        rng = np.random.default_rng(2)
+        _sample_groups_vs_oracle(oracle, key, 0, col, [0, G - 2] + rng.integers(0, G, 2).tolist(), T)
+        keep = col[:, 4242].clone()
+        col.zero_()
+        gen.init_counter(key, 0, N)
+        gen.generate_colmajor(T // 2, col[: T // 2])
+        gen.generate_colmajor(T - T // 2, col[T // 2:])
+        torch.cuda.synchronize()
+        assert gen.checksum() == csum and torch.equal(col[:, 4242], keep)
+        gen.set_stream(None)
+    del col
+    torch.cuda.empty_cache()
+
+
+def test_c3_full_size_rowmajor(pkg, golden, oracle, torch_cuda):
+    """BASELINE config 3 at its FULL size -- 2^24 instances x 64 Kbit, 137 GB of row-major keystream: checksum equal
+    to the column-major run of the same instances (layout independence), sampled rows bit-exact vs the oracle."""
+    torch = torch_cuda
+    N, T = 1 << 24, 65536
+    if _free_gib(torch) < N * T / 8 / 2**30 + 20:
+        pytest.skip("needs 137 GB of free HBM")
+    key = bytes.fromhex(golden["kats"][0]["key"])
+    first = 1 << 33
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stream(torch.cuda.current_stream().cuda_stream)
+        buf = torch.empty(N * T // 8, dtype=torch.uint8, device="cuda")
+        rows = buf.view(N, T // 8)
+        gen.init_counter(key, first, N)
+        gen.generate_rowmajor(T, rows)
+        torch.cuda.synchronize()
+        c_row = gen.checksum()
+        rng = np.random.default_rng(3)
+        for n in [0, 1023, 1024, N - 1] + rng.integers(0, N, 8).tolist():
+            keys, ivs = oracle.counter_material(key, first + int(n), 1)
+            assert rows[n].cpu().numpy().tobytes() == oracle.bulk_rowmajor(keys, ivs, 80, T)[0].tobytes(), n
+        gen.init_counter(key, first, N)
+        gen.generate_colmajor(T, buf.view(torch.int32).view(T, N // 32))   # same bytes, reused as [T][G]
+        torch.cuda.synchronize()
+        assert gen.checksum() == c_row
+        gen.set_stream(None)
+    del rows, buf
+    torch.cuda.empty_cache()
+
+
+def test_c5_full_size_fresh_material(pkg, oracle, torch_cuda):
+    """BASELINE config 5 at its FULL size -- 2^26 fresh (key, IV) pairs x 1 Kbit, explicit material arrays on the
+    device, 8.6 GB of row-major keystream: init + generate and the one-shot bulk call (28 pipeline blocks) agree on
+    every byte and on the checksum; sampled rows bit-exact vs the oracle."""
+    torch = torch_cuda
+    N, T = 1 << 26, 1024
+    if _free_gib(torch) < 2 * N * T / 8 / 2**30 + 12:
+        pytest.skip("needs 30 GB of free HBM")
+    g = torch.Generator(device="cuda").manual_seed(0x190904750)
+    keys = torch.randint(0, 256, (N, 10), dtype=torch.uint8, device="cuda", generator=g)
+    ivs = torch.randint(0, 256, (N, 10), dtype=torch.uint8, device="cuda", generator=g)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stream(torch.cuda.current_stream().cuda_stream)
+        rows = torch.empty((N, T // 8), dtype=torch.uint8, device="cuda")
+        gen.init_material(keys, ivs, 80)
+        gen.generate_rowmajor(T, rows)
+        torch.cuda.synchronize()
+        csum = gen.checksum()
+        rng = np.random.default_rng(5)
+        idx = torch.from_numpy(np.unique(np.concatenate([[0, 31, 32, N - 1], rng.integers(0, N, 300)]))).cuda()
+        want = oracle.bulk_rowmajor(keys[idx].cpu().numpy(), ivs[idx].cpu().numpy(), 80, T)
+        assert np.array_equal(rows[idx].cpu().numpy(), want)
+        rows2 = torch.empty_like(rows)
+        _, csum2 = gen.bulk_rowmajor(keys, ivs, 80, T, rows2)
+        torch.cuda.synchronize()
+        assert csum2 == csum and torch.equal(rows, rows2)
+        gen.set_stream(None)
+    del rows, rows2, keys, ivs
+    torch.cuda.empty_cache()
+
+
 def test_rowmajor_host_output_tiles(pkg, oracle):
     """Host row-major output crosses several [chain block] x [time chunk] staging tiles."""
     N, T = 32 * 32 * 2400 + 40, 4096 + 256          # > 2 x 8 x 148 chains -> two chain blocks
