@@ -234,7 +234,9 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
     if (ctx->chunk_user) {
         p.chunk = round_chunk(ctx->chunk_user);
     } else if (chains >= 2 * workers || chains <= workers) {
-        p.chunk = round_chunk(std::min<uint64_t>(T, chains <= workers ? T : 4096));
+        // Grain row-major: longer chunks (fewer state reloads at 37 LOP3 per clock; measured 9.9 -> 10.1 Tb/s)
+        const uint64_t many = rowmajor && ctx->cipher == 1 ? 16384 : 4096;
+        p.chunk = round_chunk(std::min<uint64_t>(T, chains <= workers ? T : many));
     } else {
         // workers < chains < 2 x workers: pick K for the least idle time in the last round
         const uint64_t kmax = std::max<uint64_t>(1, std::min<uint64_t>(128, T / 1024));

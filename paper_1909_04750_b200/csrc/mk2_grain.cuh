@@ -332,7 +332,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     realign<1>(b, s);
                 }
                 hs.fold(a);
-                row_drain<ALIGNED16, TG, TS, LSB>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
+                row_drain<ALIGNED16, TG, TS, LSB, 1>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);  // L2 evict_last stores
             }
             store_state(state_out, acc_out, G, g, b, s, a);
         }

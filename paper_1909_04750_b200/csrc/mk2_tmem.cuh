@@ -124,8 +124,8 @@ __device__ __forceinline__ void row_drain(uint32_t tcol, uint8_t *dst, uint64_t 
                 }
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq)
-                    *reinterpret_cast<uint4 *>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half) =
-                        make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]);
+                    store16<0>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half,
+                                              make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]));
             }
         }
     } else {

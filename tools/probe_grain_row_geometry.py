@@ -6,7 +6,7 @@ rng = np.random.default_rng(1)
 keys = torch.from_numpy(rng.integers(0, 256, (n, 10), dtype=np.uint8)).cuda()
 ivs = torch.from_numpy(rng.integers(0, 256, (n, 8), dtype=np.uint8)).cuda()
 out = torch.empty((n, T // 8), dtype=torch.uint8, device="cuda")
-for block, chunk in ((0, 0), (192, 16384), (160, 4096), (160, 16384), (128, 4096), (128, 16384), (128, 65536), (96, 16384), (0, 0)):
+for block, chunk in ((0, 0), (224, 4096), (224, 16384), (224, 65536), (192, 16384), (0, 0)):
     gen = grain.GrainGenerator(0)
     gen.set_block_threads(block); gen.set_chunk_clocks(chunk)
     gen.init_material(keys, ivs)
