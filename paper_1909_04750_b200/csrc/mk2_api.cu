@@ -804,7 +804,9 @@ static int derive_to_device(mk2_ctx *ctx, const uint8_t seed[32], uint32_t tag, 
     CK(cudaMemcpyAsync(d_seed, seed, 32, cudaMemcpyHostToDevice, ctx->stream));
     seed_setup_kernel<<<1, 256, 0, ctx->stream>>>(static_cast<const uint8_t *>(d_seed), static_cast<uint32_t *>(d_rk));
     CK(cudaGetLastError());
-    seed_derive_kernel<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(static_cast<const uint32_t *>(d_rk), tag,
+    // grid-stride kernel: six 256-thread CTAs per SM (32 KB of table each) cover any N
+    const unsigned derive_grid = (unsigned)std::min<uint64_t>((N + 255) / 256, 6ull * (uint64_t)ctx->sm_count);
+    seed_derive_kernel<<<derive_grid, 256, 0, ctx->stream>>>(static_cast<const uint32_t *>(d_rk), tag,
                                                                              first_lane, N, d_keys, d_ivs);
     CK(cudaGetLastError());
     ctx->last_launches += 2;

@@ -10,7 +10,8 @@
 // AES-128 is plain FIPS-197 (the reference's AesScalarTable,
 // pkg/src/slicerng/aes_ctr.py:193-219): byte i of a block is state row i % 4,
 // column i / 4.  The S-box is computed once per CTA into shared memory from the
-// GF(2^8) inverse + affine map, so no table literal is carried in the source.
+// GF(2^8) inverse + affine map, so no table literal is carried in the source; the
+// per-lane kernel runs on a bank-replicated SubBytes + MixColumns table built from it.
 #pragma once
 #include <cstdint>
 
@@ -88,6 +89,47 @@ __device__ __forceinline__ void aes_encrypt_block(const uint8_t *sbox, const uin
     }
 }
 
+// The bulk path: the same block function on a combined SubBytes + MixColumns table.
+//   T0[x] = (2 s, s, s, 3 s) as bytes 0..3 with s = sbox[x]: the MixColumns image of a row-0 byte; a byte of
+//   row k contributes T0 rotated left by k bytes, so one 256-word table and three rotations replace four.
+// The table is replicated 32 times in shared memory -- entry x of lane l lives at word 32 x + l, i.e. always in
+// bank l -- so the 16 data-dependent lookups of a round never conflict (the byte-wide S-box above is 64 words
+// for 32 lanes).  `tbl` points at this lane's column.
+__device__ __forceinline__ uint32_t rotl8(uint32_t w, int k) { return k ? __funnelshift_l(w, w, 8 * k) : w; }
+template <int K>
+__device__ __forceinline__ uint32_t tt(const uint32_t *tbl, uint32_t word)
+{
+    // byte K of `word`, times 32 words: (word >> 8 K & 0xFF) << 5
+    const uint32_t off = K == 0 ? (word << 5) & 0x1FE0u : (word >> (8 * K - 5)) & 0x1FE0u;
+    return tbl[off];
+}
+__device__ __forceinline__ void aes_encrypt_block_tt(const uint32_t *tbl, const uint32_t *rk /*[44]*/, uint32_t (&st)[4])
+{
+#pragma unroll
+    for (int c = 0; c < 4; ++c) st[c] ^= rk[c];
+#pragma unroll 1
+    for (int r = 1; r < 10; ++r) {
+        uint32_t t[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)  // row k of output column c comes from column (c + k) & 3 (ShiftRows)
+            t[c] = tt<0>(tbl, st[c]) ^ rotl8(tt<1>(tbl, st[(c + 1) & 3]), 1) ^ rotl8(tt<2>(tbl, st[(c + 2) & 3]), 2) ^
+                   rotl8(tt<3>(tbl, st[(c + 3) & 3]), 3) ^ rk[4 * r + c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) st[c] = t[c];
+    }
+    uint32_t t[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {  // last round: SubBytes + ShiftRows only; s is byte 1 of T0
+        const uint32_t b0 = (tt<0>(tbl, st[c]) >> 8) & 0xFFu;
+        const uint32_t b1 = tt<1>(tbl, st[(c + 1) & 3]) & 0xFF00u;
+        const uint32_t b2 = (tt<2>(tbl, st[(c + 2) & 3]) << 8) & 0xFF0000u;
+        const uint32_t b3 = (tt<3>(tbl, st[(c + 3) & 3]) << 16) & 0xFF000000u;
+        t[c] = (b0 | b1 | b2 | b3) ^ rk[40 + c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) st[c] = t[c];
+}
+
 // 1 thread: derivation key and its round keys (as little-endian column words).
 __global__ void seed_setup_kernel(const uint8_t *__restrict__ seed /*[32]*/, uint32_t *__restrict__ rk_out /*[44]*/)
 {
@@ -121,29 +163,43 @@ __global__ void __launch_bounds__(256)
 seed_derive_kernel(const uint32_t *__restrict__ rk_in, uint32_t tag, uint64_t first_lane, uint64_t n,
                    uint8_t *__restrict__ keys, uint8_t *__restrict__ ivs)
 {
-    __shared__ uint8_t sbox[256];
+    __shared__ uint32_t t0r[256 * 32];  // T0, one copy per bank (32 KB)
     __shared__ uint32_t rk[44];
-    for (int x = threadIdx.x; x < 256; x += blockDim.x) sbox[x] = aes_sbox_compute((uint8_t)x);
+    for (int x = threadIdx.x; x < 256; x += blockDim.x) {
+        const uint32_t sb = aes_sbox_compute((uint8_t)x), s2 = gf_xtime((uint8_t)sb);
+        const uint32_t w = s2 | (sb << 8) | (sb << 16) | ((s2 ^ sb) << 24);
+        for (int l = 0; l < 32; ++l) t0r[32 * x + l] = w;
+    }
     if (threadIdx.x < 44) rk[threadIdx.x] = rk_in[threadIdx.x];
     __syncthreads();
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const uint32_t lane = (uint32_t)(first_lane + j);
-    uint32_t stream[8];
+    const uint32_t *tbl = t0r + (threadIdx.x & 31);
+    const bool even = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(ivs)) & 1u) == 0;
+    // grid-stride over lanes: the table build (an S-box inversion per thread) is paid once per CTA, not per 256 lanes
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t lane = (uint32_t)(first_lane + j);
+        uint32_t stream[8];
 #pragma unroll
-    for (uint32_t c = 0; c < 2; ++c) {
-        // bytes: [tag, lane>>24, lane>>16, lane>>8 | lane, 0, 0, 0 | c, 0, 0, 0 | 0, 0, 0, 0]
-        uint32_t st[4] = {tag | ((lane >> 24) << 8) | (((lane >> 16) & 0xFF) << 16) | (((lane >> 8) & 0xFF) << 24),
-                          lane & 0xFF, c, 0u};
-        aes_encrypt_block(sbox, rk, st);
+        for (uint32_t c = 0; c < 2; ++c) {
+            // bytes: [tag, lane>>24, lane>>16, lane>>8 | lane, 0, 0, 0 | c, 0, 0, 0 | 0, 0, 0, 0]
+            uint32_t st[4] = {tag | ((lane >> 24) << 8) | (((lane >> 16) & 0xFF) << 16) | (((lane >> 8) & 0xFF) << 24),
+                              lane & 0xFF, c, 0u};
+            aes_encrypt_block_tt(tbl, rk, st);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) stream[4 * c + w] = st[w];
+            for (int w = 0; w < 4; ++w) stream[4 * c + w] = st[w];
+        }
+        uint8_t *k = keys + 10 * j, *v = ivs + 10 * j;
+        if (even) {  // 10-byte records at even addresses: five 16-bit stores each instead of ten byte stores
+#pragma unroll
+            for (int u = 0; u < 5; ++u) reinterpret_cast<uint16_t *>(k)[u] = (uint16_t)(stream[u >> 1] >> (16 * (u & 1)));
+#pragma unroll
+            for (int u = 5; u < 10; ++u) reinterpret_cast<uint16_t *>(v)[u - 5] = (uint16_t)(stream[u >> 1] >> (16 * (u & 1)));
+        } else {
+#pragma unroll
+            for (int b = 0; b < 10; ++b) k[b] = (uint8_t)(stream[b >> 2] >> (8 * (b & 3)));
+#pragma unroll
+            for (int b = 10; b < 20; ++b) v[b - 10] = (uint8_t)(stream[b >> 2] >> (8 * (b & 3)));
+        }
     }
-    uint8_t *k = keys + 10 * j, *v = ivs + 10 * j;
-#pragma unroll
-    for (int b = 0; b < 10; ++b) k[b] = (uint8_t)(stream[b >> 2] >> (8 * (b & 3)));
-#pragma unroll
-    for (int b = 10; b < 20; ++b) v[b - 10] = (uint8_t)(stream[b >> 2] >> (8 * (b & 3)));
 }
 
 }  // namespace mk2
