@@ -21,10 +21,15 @@ with pkg.MickeyGenerator(0) as gen:
     gen.generate_rowmajor(T)
     gen.clock(True, None, 3)
     gen.checksum()
+    bulk, bsum = gen.bulk_rowmajor(keys, ivs, 80, T)
+    gen.set_row_staging(1)
+    row_smem = gen.init_material(keys, ivs, 80).generate_rowmajor(T)
+    gen.set_row_staging(0)
     k2, i2 = gen.derive_material(bytes(range(32)), 5, 777)
     gen.init_seed(bytes(range(32)), 5, 777).generate_colmajor(64)
 assert np.array_equal(col, orc.bulk_colmajor(keys, ivs, 80, T))
 assert np.array_equal(row, orc.bulk_rowmajor(keys, ivs, 80, T))
+assert np.array_equal(bulk, row) and np.array_equal(row_smem, row)
 assert np.array_equal(colr, orc.bulk_colmajor(keys, ivs, nbits, T))
 wk, wi = orc.derive_material(bytes(range(32)), 5, 777)
 assert np.array_equal(k2, wk) and np.array_equal(i2, wi)
