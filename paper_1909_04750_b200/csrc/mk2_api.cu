@@ -698,7 +698,10 @@ static int init_uniform_device(mk2_ctx *ctx, const uint8_t *dk, const uint8_t *d
     uint32_t *mat = nullptr;
     const int load = (int)iv_bits + KEY_BITS;
     CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->pool, ctx->stream));
-    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, ctx->N, ctx->G, mat);
+    const bool fast10 = reinterpret_cast<uintptr_t>(dk) % 16 == 0 &&
+                        (!iv_bits || (iv_stride == 10 && reinterpret_cast<uintptr_t>(di) % 16 == 0));
+    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, ctx->N, ctx->G, mat,
+                                                                        fast10);
     CK(cudaGetLastError());
     ctx->last_launches++;
     if ((rc = launch_init(ctx, mat, load, 0, false))) return rc;
@@ -844,20 +847,12 @@ int mk2_init_from_seed(mk2_ctx *ctx, const uint8_t seed[32], uint64_t first_lane
     if (rc) return rc;
     if ((rc = begin_timing(ctx))) return rc;
     void *dk = nullptr, *di = nullptr;
-    uint32_t *mat = nullptr;
     CK(cudaMallocFromPoolAsync(&dk, N * 10, ctx->pool, ctx->stream));
     CK(cudaMallocFromPoolAsync(&di, N * 10, ctx->pool, ctx->stream));
     if ((rc = derive_to_device(ctx, seed, 3u /* mickey */, first_lane, N, static_cast<uint8_t *>(dk),
                                static_cast<uint8_t *>(di))))
         return rc;
-    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)160 * ctx->G, ctx->pool, ctx->stream));
-    pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(static_cast<const uint8_t *>(dk),
-                                                                       static_cast<const uint8_t *>(di), 10, 80, N,
-                                                                       ctx->G, mat);
-    CK(cudaGetLastError());
-    ctx->last_launches++;
-    if ((rc = launch_init(ctx, mat, 160, 0, false))) return rc;
-    CK(cudaFreeAsync(mat, ctx->stream));
+    if ((rc = init_uniform_device(ctx, static_cast<const uint8_t *>(dk), static_cast<const uint8_t *>(di), 10, 80))) return rc;
     CK(cudaFreeAsync(dk, ctx->stream));
     CK(cudaFreeAsync(di, ctx->stream));
     return end_timing(ctx);
