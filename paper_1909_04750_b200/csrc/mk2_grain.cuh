@@ -22,6 +22,10 @@ namespace mk2 {
 namespace grain {
 
 constexpr int GB = 80;           // bits per register (grain.py:29)
+#ifndef MK2_GRAIN_STORE_POLICY
+#define MK2_GRAIN_STORE_POLICY 2
+#endif
+constexpr int GRAIN_STORE_POLICY = MK2_GRAIN_STORE_POLICY;  // row stores: 1 = 2 x 16 B, 2 = 1 x 32 B, both L2 evict_last
 constexpr int WIN = 16;          // clocks per window realignment
 constexpr int GW = GB + WIN;     // window length
 constexpr int INIT_CLOCKS = 160; // grain.py:30
@@ -332,7 +336,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     realign<1>(b, s);
                 }
                 hs.fold(a);
-                row_drain<ALIGNED16, TG, TS, LSB, 1>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);  // L2 evict_last stores
+                row_drain<ALIGNED16, TG, TS, LSB, GRAIN_STORE_POLICY>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
             }
             store_state(state_out, acc_out, G, g, b, s, a);
         }

@@ -732,6 +732,16 @@ __device__ __forceinline__ void store16(uint8_t *p, uint4 v)
     }
 }
 
+// One 32-byte (256-bit, sm_100) row store with the same L2 hint: a whole sector in a single request.
+__device__ __forceinline__ void store32_keep(uint8_t *p, const uint32_t (&v)[8])
+{
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(pol)
+                 : "memory");
+}
+
 // Drain of one staging tile (ngrp 8-clock groups of keystream words in the thread's smem
 // column `col`, stride TS) into the instance rows at `dst`.  Shared by every cipher's
 // row-major kernel.  LSB selects the byte packing: first bit in the MSB (library default,
@@ -764,7 +774,26 @@ __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t 
     }
     // ---- pass 2: TG bytes (or the tail) per instance row, 16 bytes per store; the two
     // halves of a 32-byte sector are stored back to back so they merge in L2
-    if (ALIGNED16 && ngrp == TG && nrows == 32) {
+    if (STORE_POLICY == 2 && TG == 32 && ALIGNED16 && ngrp == TG && nrows == 32 &&
+        ((reinterpret_cast<uintptr_t>(dst) | pitch) & 31) == 0) {
+        // whole 32-byte sectors in one store each
+#pragma unroll 1
+        for (int kk = 0; kk < 8; ++kk) {
+            uint32_t y[8][4];  // [g4][q]
+#pragma unroll
+            for (int g4 = 0; g4 < 8; ++g4) {
+                uint32_t x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = col[((4 * g4 + u) * 8 + kk) * ts];
+                bytes4x4(x, y[g4]);
+            }
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const uint32_t v[8] = {y[0][qq], y[1][qq], y[2][qq], y[3][qq], y[4][qq], y[5][qq], y[6][qq], y[7][qq]};
+                store32_keep(dst + (uint64_t)(8 * qq + kk) * pitch, v);
+            }
+        }
+    } else if (ALIGNED16 && ngrp == TG && nrows == 32) {
 #pragma unroll 1
         for (int kk = 0; kk < 8; ++kk) {
 #pragma unroll DRAIN_UNROLL_HALF
@@ -779,7 +808,7 @@ __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t 
                 }
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq)
-                    store16<STORE_POLICY>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half,
+                    store16<(STORE_POLICY != 0)>(dst + (uint64_t)(8 * qq + kk) * pitch + 16 * half,
                                               make_uint4(y[0][qq], y[1][qq], y[2][qq], y[3][qq]));
             }
         }
