@@ -451,6 +451,97 @@ uint64_t mk2o_checksum_colmajor(const uint32_t *out, uint64_t T, uint64_t G, uin
 }
 
 /* ------------------------------------------------------------------------
+ * The same checksum for a whole job, WITHOUT materialising the keystream, so
+ * that BASELINE-size geometries (2^20 instances, every chain) can be checked
+ * instance by instance: mk2o_checksum_colmajor(mk2o_bulk_colmajor(...)) computed
+ * batch by batch (64 lanes = one call of kernels.mickey_sliced_words,
+ * kernels.py:189-200, as the reference's callers batch, cli.py:219-231).
+ *   counter != 0: the synthetic set of SURVEY.md 8(d) -- every lane uses
+ *       keys[0..9], lane n gets the 80-bit big-endian IV (first + n); ivs is
+ *       ignored and first must be a multiple of 64;
+ *   counter == 0: explicit material, arguments as mk2o_bulk_colmajor.
+ * g_offset: global group index of group 0 (the weight 2^(32 ((g+g_offset)&1))).
+ * *rc: 0, or -1 (allocation / thread failure).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const uint8_t *keys, *ivs, *iv_nbits;
+    int iv_stride, iv_uniform, counter;
+    uint64_t first, N, T, G, nb, g_offset;
+    uint64_t next; /* atomic */
+    uint64_t sum;  /* atomic */
+    int fail;
+} csum_job;
+
+static void *csum_worker(void *arg)
+{
+    csum_job *jb = (csum_job *)arg;
+    const uint64_t T = jb->T;
+    uint64_t *words = (uint64_t *)malloc((T + 2) * sizeof(uint64_t));
+    if (!words) {
+        __atomic_store_n(&jb->fail, 1, __ATOMIC_RELAXED);
+        return NULL;
+    }
+    uint64_t local = 0;
+    for (;;) {
+        const uint64_t b = __atomic_fetch_add(&jb->next, 1, __ATOMIC_RELAXED);
+        if (b >= jb->nb) break;
+        const uint64_t lane0 = b * 64;
+        if (jb->counter) {
+            /* all 64 lanes of the batch continue the counter, also past N: mk2_init_counter_iv synthesises
+             * whole 32-lane groups (groups past G are dropped from the sum below) */
+            const int n = 64;
+            uint8_t k64[64 * 10], v64[64 * 10];
+            for (int j = 0; j < n; ++j) {
+                const uint64_t idx = jb->first + lane0 + (uint64_t)j;
+                memcpy(k64 + 10 * j, jb->keys, 10);
+                v64[10 * j] = v64[10 * j + 1] = 0;
+                for (int q = 0; q < 8; ++q) v64[10 * j + 2 + q] = (uint8_t)(idx >> (8 * (7 - q)));
+            }
+            batch_words(k64, v64, 10, NULL, 80, 0, (uint64_t)n, T, words);
+        } else {
+            batch_words(jb->keys, jb->ivs, jb->iv_stride, jb->iv_nbits, jb->iv_uniform, lane0, jb->N, T, words);
+        }
+        const uint64_t g0 = 2 * b;
+        const int has_hi = g0 + 1 < jb->G;
+        const int odd = (int)((g0 + jb->g_offset) & 1);
+        uint64_t lo = 0, hi = 0;
+        for (uint64_t t = 0; t < T; ++t) {
+            lo += (uint32_t)words[t];
+            hi += words[t] >> 32;
+        }
+        if (!has_hi) hi = 0;
+        local += odd ? (lo << 32) + hi : lo + (hi << 32);
+    }
+    free(words);
+    __atomic_fetch_add(&jb->sum, local, __ATOMIC_RELAXED);
+    return NULL;
+}
+
+uint64_t mk2o_checksum_job(const uint8_t *keys, const uint8_t *ivs, int iv_stride, const uint8_t *iv_nbits,
+                           int iv_uniform, int counter, uint64_t first, uint64_t N, uint64_t T, uint64_t g_offset,
+                           int nthreads, int *rc)
+{
+    csum_job jb = {keys, ivs, iv_nbits, iv_stride, iv_uniform, counter, first, N, T, (N + 31) / 32, (N + 63) / 64,
+                   g_offset, 0, 0, 0};
+    build_masks();
+    if (nthreads < 1) nthreads = mk2o_max_threads();
+    if ((uint64_t)nthreads > jb.nb) nthreads = (int)(jb.nb ? jb.nb : 1);
+    if (nthreads > 1024) nthreads = 1024;
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    int started = 0;
+    if (th)
+        for (int i = 0; i < nthreads; ++i) {
+            if (pthread_create(&th[i], NULL, csum_worker, &jb) != 0) break;
+            ++started;
+        }
+    if (started == 0) csum_worker(&jb); /* degrade to the calling thread */
+    for (int i = 0; i < started; ++i) pthread_join(th[i], NULL);
+    free(th);
+    if (rc) *rc = jb.fail ? -1 : 0;
+    return jb.sum;
+}
+
+/* ------------------------------------------------------------------------
  * Seed derivation: pkg/src/slicerng/seedgen.py:57-86.
  * AES-128 is the standard FIPS-197 cipher the reference implements as
  * AesScalarTable (pkg/src/slicerng/aes_ctr.py:193-219); restated here with a

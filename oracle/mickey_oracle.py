@@ -59,6 +59,9 @@ def lib() -> C.CDLL:
         L.mk2o_timed_loops.restype = C.c_uint64
         L.mk2o_checksum_colmajor.argtypes = [u32p, C.c_uint64, C.c_uint64, C.c_uint64]
         L.mk2o_checksum_colmajor.restype = C.c_uint64
+        L.mk2o_checksum_job.argtypes = [u8p, u8p, C.c_int, u8p, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        C.c_uint64, C.c_int, C.POINTER(C.c_int)]
+        L.mk2o_checksum_job.restype = C.c_uint64
         L.mk2o_max_threads.restype = C.c_int
         L.mk2o_aes128_encrypt.argtypes = [u8p, u8p, u8p]
         L.mk2o_grain_init.argtypes = [C.c_void_p, u8p, u8p, C.c_int]
@@ -233,6 +236,32 @@ def checksum_colmajor(out: np.ndarray, g_offset: int = 0) -> int:
     out = np.ascontiguousarray(out, np.uint32)
     T, G = out.shape
     return int(lib().mk2o_checksum_colmajor(_p(out, u32p), T, G, g_offset))
+
+
+def checksum_counter(key: bytes, first: int, n: int, T: int, g_offset: int | None = None, nthreads: int = 0) -> int:
+    """Checksum of the whole counter-IV job (SURVEY.md 8(d) set: one key, IV_k = 80-bit big-endian k for
+    k = first .. first+n-1, T bits each) computed batch by batch without materialising the keystream:
+    equals checksum_colmajor(bulk_colmajor(*counter_material(key, first, n), 80, T), first // 32)."""
+    if first % 64:
+        raise ValueError("first must be a multiple of 64")
+    k = np.frombuffer(bytes(key), np.uint8).copy()
+    rc = C.c_int(0)
+    v = lib().mk2o_checksum_job(_p(k, u8p), None, 10, None, 80, 1, first, n, T,
+                                first // 32 if g_offset is None else g_offset, nthreads, C.byref(rc))
+    if rc.value:
+        raise RuntimeError(f"oracle checksum_counter rc={rc.value}")
+    return int(v)
+
+
+def checksum_material(keys, ivs, iv_bits, T: int, g_offset: int = 0, nthreads: int = 0) -> int:
+    """Checksum of bulk_colmajor(keys, ivs, iv_bits, T) without materialising it (every instance, every bit)."""
+    keys, ivs, uniform, nb, N = _bulk_args(keys, ivs, iv_bits)
+    rc = C.c_int(0)
+    v = lib().mk2o_checksum_job(_p(keys, u8p), _p(ivs, u8p), ivs.shape[1], _p(nb, u8p), uniform, 0, 0, N, T, g_offset,
+                                nthreads, C.byref(rc))
+    if rc.value:
+        raise RuntimeError(f"oracle checksum_material rc={rc.value}")
+    return int(v)
 
 
 def counter_material(key: bytes, first: int, n: int):

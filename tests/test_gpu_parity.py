@@ -379,6 +379,124 @@ def test_c2_instance_count_sampled_and_checksummed(pkg, golden, oracle, torch_cu
         gen.set_stream(None)
 
 
+def _rowmajor_buffer_checksum(torch, rows, g_offset=0):
+    """The checksum (sum of the column-major stream as u64 words) recomputed from a ROW-major device buffer:
+    sum_n popcount(row n) << ((n + 32 g_offset) % 64), mod 2^64."""
+    lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=rows.device)
+    N = rows.shape[0]
+    total = 0
+    step = max(1, (1 << 25) // max(1, rows.shape[1]))
+    for n0 in range(0, N, step):
+        blk = rows[n0:n0 + step]
+        pc = lut[blk.long()].sum(dim=1)
+        sh = (torch.arange(n0, n0 + blk.shape[0], device=rows.device, dtype=torch.int64) + 32 * (g_offset & 1)) % 64
+        total = (total + int(torch.bitwise_left_shift(pc, sh).sum().item())) % (1 << 64)
+    return total
+
+
+def test_full_coverage_checksum_c2_geometry(pkg, golden, oracle, torch_cuda):
+    """EVERY instance and chain of the BASELINE config 2 geometry (2^20 instances = 1024 chains) against the oracle:
+    the oracle computes the checksum of the whole 2^20 x 4096-bit job batch by batch (mk2o_checksum_job, pinned to the
+    reference's own wrap-sums in tests/test_oracle.py); the GPU's in-kernel checksum must equal it in both layouts,
+    and must equal the sum of the buffer it emitted (so the emitted bits, not just the accumulators, are covered).
+    Mirrors tests/test_acceptance.py:103-135 (all instances compared, not a sample)."""
+    torch = torch_cuda
+    key = bytes.fromhex(golden["kats"][0]["key"])
+    N, T = 1 << 20, 4096
+    G = N // 32
+    first = 3 << 20
+    want = oracle.checksum_counter(key, first, N, T)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stream(torch.cuda.current_stream().cuda_stream)
+        gen.set_group_offset(first // 32)
+        gen.init_counter(key, first, N)
+        col = torch.empty((T, G), dtype=torch.int32, device="cuda")
+        gen.generate_colmajor(T, col)
+        torch.cuda.synchronize()
+        assert gen.checksum() == want
+        assert int(col.view(torch.int64).sum().item()) % (1 << 64) == want
+        del col
+        gen.init_counter(key, first, N)
+        rows = torch.empty((N, T // 8), dtype=torch.uint8, device="cuda")
+        gen.generate_rowmajor(T, rows)
+        torch.cuda.synchronize()
+        assert gen.checksum() == want
+        assert _rowmajor_buffer_checksum(torch, rows, first // 32) == want
+        gen.set_stream(None)
+    del rows
+    torch.cuda.empty_cache()
+
+
+def test_full_coverage_checksum_c3_clock_count(pkg, golden, oracle, torch_cuda):
+    """BASELINE config 3's clock count (65 536 bits per instance, 16 scheduling chunks with state parking in
+    between) for every one of 2^18 instances, row-major through tensor memory and column-major, against the
+    oracle's whole-job checksum."""
+    torch = torch_cuda
+    key = bytes.fromhex(golden["kats"][0]["key"])
+    N, T = 1 << 18, 65536
+    first = 1 << 33
+    want = oracle.checksum_counter(key, first, N, T)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stream(torch.cuda.current_stream().cuda_stream)
+        gen.set_group_offset(first // 32)
+        buf = torch.empty(N * T // 8, dtype=torch.uint8, device="cuda")
+        gen.init_counter(key, first, N)
+        gen.generate_rowmajor(T, buf.view(N, T // 8))
+        torch.cuda.synchronize()
+        assert gen.checksum() == want
+        assert _rowmajor_buffer_checksum(torch, buf.view(N, T // 8), first // 32) == want
+        gen.init_counter(key, first, N)
+        col = buf.view(torch.int32).view(T, N // 32)
+        gen.generate_colmajor(T, col)
+        torch.cuda.synchronize()
+        assert gen.checksum() == want
+        assert int(col.view(torch.int64).sum().item()) % (1 << 64) == want
+        gen.set_stream(None)
+    del buf, col
+    torch.cuda.empty_cache()
+
+
+def test_full_coverage_checksum_c5_explicit_material(pkg, oracle, torch_cuda):
+    """BASELINE config 5's shape (fresh random key/IV pairs x 1 Kbit) for every one of 2^20 pairs: explicit host
+    material through mk2_init_from_material + generate and through the one-shot mk2_bulk_rowmajor (several
+    pipeline blocks), both against the oracle's whole-job checksum."""
+    N, T = 1 << 20, 1024
+    rng = np.random.default_rng(0x1909)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    want = oracle.checksum_material(keys, ivs, 80, T)
+    with pkg.MickeyGenerator(0) as gen:
+        col = gen.init_material(keys, ivs, 80).generate_colmajor(T)
+        assert gen.checksum() == want
+        assert int(col.view("<u8").sum(dtype=np.uint64)) == want
+        rows, csum = gen.bulk_rowmajor(keys, ivs, 80, T)
+        assert csum == want
+        bits = np.unpackbits(rows[4096:4160], axis=1)              # rows -> column words of one 64-lane batch
+        words = (bits.T.astype(np.uint64) << np.arange(64, dtype=np.uint64)).sum(axis=1, dtype=np.uint64)
+        assert np.array_equal(words, col[:, 128:130].copy().view("<u8").reshape(-1))
+
+
+def test_full_length_chains_every_group(pkg, golden, oracle, torch_cuda):
+    """The full 10^6-clock length of BASELINE config 2 (15 scheduling chunks, state parked and reloaded between
+    them) for EVERY group of 32 chains (2^15 instances), against the oracle's whole-job checksum."""
+    torch = torch_cuda
+    key = bytes.fromhex(golden["kats"][0]["key"])
+    N, T = 1 << 15, 1_000_000
+    want = oracle.checksum_counter(key, 0, N, T)
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stream(torch.cuda.current_stream().cuda_stream)
+        gen.set_chunk_clocks(66688)                                # the chunk length the planner picks at 2^20 instances
+        gen.init_counter(key, 0, N)
+        col = torch.empty((T, N // 32), dtype=torch.int32, device="cuda")
+        gen.generate_colmajor(T, col)
+        torch.cuda.synchronize()
+        assert gen.checksum() == want
+        assert int(col.view(torch.int64).sum().item()) % (1 << 64) == want
+        gen.set_stream(None)
+    del col
+    torch.cuda.empty_cache()
+
+
 def _free_gib(torch):
     torch.cuda.empty_cache()
     return torch.cuda.mem_get_info()[0] / 2**30

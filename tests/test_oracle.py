@@ -184,3 +184,26 @@ def test_grain_oracle_matches_reference(oracle, golden):
     assert sha(oracle.grain_bulk_colmajor(keys, ivs, T).tobytes()) == g["long"]["words_u8_sha256"]
     assert sha(oracle.grain_bulk_rowmajor(keys, ivs, T).tobytes()) == g["long"]["lane_major_msb_sha256"]
     assert sha(oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb").tobytes()) == g["long"]["lane_major_lsb_sha256"]
+
+
+def test_whole_job_checksum_matches_reference_and_buffer_checksum(oracle, golden):
+    """mk2o_checksum_job (the full-coverage checker of the BASELINE-size GPU tests) against the reference's own
+    uint64 wrap-sums of the counter-IV sets, and against the checksum of the materialised oracle buffer."""
+    for rec in golden["counter_iv"]:
+        key = bytes.fromhex(rec["key"])
+        assert f"{oracle.checksum_counter(key, rec['first'], rec['n'], rec['nclocks']):016x}" == rec["u64_wrap_sum"].rjust(16, "0")
+    key = bytes.fromhex("123456789abcdef01234")
+    for first, n, T in ((0, 64, 100), (64, 96, 77), (128, 992, 33), (0, 32, 8)):
+        k, v = oracle.counter_material(key, first, n)
+        want = oracle.checksum_colmajor(oracle.bulk_colmajor(k, v, 80, T), first // 32)
+        assert oracle.checksum_counter(key, first, n, T) == want
+        assert oracle.checksum_counter(key, first, n, T, nthreads=1) == want
+    rng = np.random.default_rng(3)
+    for n, T, ivb, go in ((1000, 65, 80, 0), (64, 12, 13, 1), (33, 9, 0, 3)):
+        k = rng.integers(0, 256, (n, 10), dtype=np.uint8)
+        v = rng.integers(0, 256, (n, 10), dtype=np.uint8)
+        assert oracle.checksum_material(k, v, ivb, T, go) == oracle.checksum_colmajor(oracle.bulk_colmajor(k, v, ivb, T), go)
+    nb = rng.integers(0, 81, 1000).astype(np.uint8)   # ragged IV lengths
+    k = rng.integers(0, 256, (1000, 10), dtype=np.uint8)
+    v = rng.integers(0, 256, (1000, 10), dtype=np.uint8)
+    assert oracle.checksum_material(k, v, nb, 40) == oracle.checksum_colmajor(oracle.bulk_colmajor(k, v, nb, 40))
