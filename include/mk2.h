@@ -15,8 +15,22 @@
  * owns one group (32 instances, column-major: one 32-bit word per bit of the
  * 100-bit R and S registers -- MickeySliced, pkg/src/slicerng/mickey.py:236).
  * Pointers marked "host or device" are classified with
- * cudaPointerGetAttributes; device pointers are used in place (e.g. a torch
- * CUDA tensor's data_ptr()), host pointers are staged through pinned buffers.
+ * cudaPointerGetAttributes:
+ *   device pointers  are used in place (e.g. a torch CUDA tensor's data_ptr());
+ *   pinned host      (cudaHostAlloc / cudaHostRegister / mk2_host_alloc /
+ *                    torch pin_memory) outputs receive asynchronous D2H copies
+ *                    of the device staging tiles directly, at link speed;
+ *   pageable host    (malloc, a fresh numpy array) outputs go through two
+ *                    pinned bounce buffers owned by the context, and a small
+ *                    pool of host threads (mk2_set_host_threads) moves each
+ *                    bounce tile into the caller's array while the next tile
+ *                    crosses the link; pageable inputs (key/IV bytes, 20 B per
+ *                    instance) are plain cudaMemcpyAsync calls.
+ * Every output call returns with the caller's array complete.
+ *
+ * Current device: every entry point runs on its context's device and restores
+ * the caller's current CUDA device before it returns, so a process that drives
+ * other devices (e.g. torch on cuda:0, a context on device 1) is not disturbed.
  *
  * Threading: a context is exclusively owned by one thread at a time
  * (SPEC.md:336-337 gives the reference's engines the same rule); use one
@@ -46,7 +60,7 @@ enum {
 #define MK2_IV_UNUSED 0xFFu /* mk2_init_ragged: lane stays in the all-zero state */
 
 /* Library / device discovery. */
-int mk2_abi_version(void); /* currently 1 */
+int mk2_abi_version(void); /* currently 2 */
 int mk2_device_count(void);
 
 /* Context = one device, one stream, the state of N instances. */
@@ -102,10 +116,12 @@ int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_inde
  * AES-128 counter construction under a key derived from the 32-byte master
  * seed; lane n gets key = stream[0:10], iv = stream[10:20].  The reference caps
  * a seed at 64 lanes (seedgen.py:22); here first_lane + N may be up to 2^32
- * (the lane field of the derivation block).  algo_tag: 1 aes-ctr, 2 grain,
- * 3 mickey (seedgen.py:31).  mk2_derive_material writes keys/ivs (N x 10 bytes
- * each, host or device); mk2_init_from_seed derives (tag 3) and initialises in
- * one go without the material ever leaving the device.
+ * (the lane field of the derivation block).  algo_tag (seedgen.py:24-31):
+ * 3 = mickey, keys N x 10 and ivs N x 10 bytes; 2 = grain, keys N x 10 and ivs
+ * N x 8 bytes (stream[10:18]).  Tag 1 (aes-ctr, 16-byte key + 12-byte nonce) and
+ * unknown tags are rejected with MK2_E_ARG: that cipher is not on this library's
+ * path.  keys / ivs: host or device.  mk2_init_from_seed derives (tag 3) and
+ * initialises in one go without the material ever leaving the device.
  */
 int mk2_derive_material(mk2_ctx *ctx, const uint8_t seed[32], uint32_t algo_tag, uint64_t first_lane, uint64_t N,
                         uint8_t *keys, uint8_t *ivs);
@@ -132,6 +148,10 @@ int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_w
  * successive calls can fill a longer row chunk by chunk.  out: host or device.
  */
 int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes);
+/* The same with the byte packing chosen by the caller: lsb_first != 0 puts the
+ * first bit of every byte in its LEAST significant position -- bit_order="lsb"
+ * of kernels.words_to_lane_bytes / words_lane_major_bytes (kernels.py:610-611). */
+int mk2_generate_rowmajor_order(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes, int lsb_first);
 
 /*
  * n raw CLOCK_KG steps without output: MickeySliced.clock_kg(mixing, word)
@@ -210,6 +230,15 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
  * in flight: one being generated, one being copied out).  0 = default (32 MiB;
  * row-major tiles, which are 2-D copies, are 16x this). */
 int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes);
+/* Host threads (the calling thread included) that move bounce tiles into
+ * PAGEABLE output arrays; 0 = automatic (half the hardware threads, 2..8). */
+int mk2_set_host_threads(mk2_ctx *ctx, int threads);
+/* Pinned (page-locked, portable) host memory for output arrays that should take
+ * the direct D2H path: what the Python front end's fresh result arrays are made
+ * of (kernels.py:194-200 returns a fresh array per call; here it comes from a
+ * cached pinned pool).  mk2_last_error(NULL) has the text after a failure. */
+int mk2_host_alloc(size_t bytes, void **out);
+int mk2_host_free(void *p);
 /* Tuning knob: where the row-major kernel parks 256 keystream words per thread
  * between two drains: 1 = shared memory (seven worker warps per SM fit),
  * 2 = tensor memory (tcgen05.st / tcgen05.ld; eight fit), 0 = automatic

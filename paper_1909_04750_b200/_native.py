@@ -17,6 +17,7 @@ _PKG = Path(__file__).resolve().parent
 _lock = threading.Lock()
 _lib = None
 
+ABI_VERSION = 2
 MK2_OK = 0
 MK2_E_CUDA, MK2_E_ARG, MK2_E_STATE, MK2_E_NODEVICE, MK2_E_NOMEM = -1, -2, -3, -4, -5
 MK2_IV_UNUSED = 0xFF
@@ -46,6 +47,10 @@ SYMBOLS = {
     "mk2_init_from_seed": (C.c_int, [_vp, _u8p, _u64, _u64]),
     "mk2_generate_colmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
     "mk2_generate_rowmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
+    "mk2_generate_rowmajor_order": (C.c_int, [_vp, _u64, _vp, _u64, C.c_int]),
+    "mk2_set_host_threads": (C.c_int, [_vp, C.c_int]),
+    "mk2_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "mk2_host_free": (C.c_int, [_vp]),
     "mk2_grain_init_from_material": (C.c_int, [_vp, _u8p, _u8p, _u64]),
     "mk2_grain_generate_colmajor": (C.c_int, [_vp, _u64, _vp, _u64]),
     "mk2_grain_generate_rowmajor": (C.c_int, [_vp, _u64, _vp, _u64, C.c_int]),
@@ -85,14 +90,17 @@ def lib() -> C.CDLL:
             import os
 
             override = os.environ.get("MK2_LIB")  # experiments: an alternative build of the same sources
-            path = Path(override) if override else _build.LIB
-            if not path.exists():
-                _build.build_native()
+            if override:
+                path = Path(override)
+            else:
+                path = _build.build_native()  # no-op unless a source changed since the library was built
             L = C.CDLL(str(path))
             for name, (res, args) in SYMBOLS.items():
                 fn = getattr(L, name)  # AttributeError = ABI mismatch, fail loudly
                 fn.restype = res
                 fn.argtypes = args
+            if L.mk2_abi_version() != ABI_VERSION:
+                raise Mk2Error(f"{path} has ABI version {L.mk2_abi_version()}, this package needs {ABI_VERSION}")
             _lib = L
     return _lib
 

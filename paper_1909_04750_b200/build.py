@@ -7,6 +7,7 @@ container; the .so is git-ignored but travels to the GPU box with the tree.
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -29,11 +30,25 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA path cannot be built (there is no CPU fallback)")
 
 
+def source_hash(sources) -> str:
+    h = hashlib.sha256()
+    for src in sorted(Path(s) for s in sources):
+        h.update(src.name.encode() + b"\0")
+        h.update(src.read_bytes())
+    return h.hexdigest()
+
+
 def _stale(target: Path, sources) -> bool:
-    if not target.exists():
+    """A library is current when the hash of the sources it was built from (written next to it) matches the
+    sources on disk.  Content, not mtimes: the tree is copied to the GPU box, and a checkout rewrites mtimes."""
+    stamp = Path(str(target) + ".srchash")
+    if not target.exists() or not stamp.exists():
         return True
-    t = target.stat().st_mtime
-    return any(Path(s).stat().st_mtime > t for s in sources)
+    return stamp.read_text().strip() != source_hash(sources)
+
+
+def _stamp(target: Path, sources) -> None:
+    Path(str(target) + ".srchash").write_text(source_hash(sources) + "\n")
 
 
 def build_native(force: bool = False, verbose: bool = False) -> Path:
@@ -47,6 +62,7 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
             print(res.stdout, file=sys.stderr)
         if res.returncode:
             raise RuntimeError("nvcc failed building libmk2.so")
+        _stamp(LIB, srcs)
     return LIB
 
 
@@ -59,6 +75,7 @@ def build_curand(force: bool = False) -> Path:
         if res.returncode:
             print(res.stdout, file=sys.stderr)
             raise RuntimeError("nvcc failed building libmk2_curand.so")
+        _stamp(CURAND_LIB, [src])
     return CURAND_LIB
 
 

@@ -59,8 +59,7 @@ def _init_grain(gen: GrainGenerator, args):
         seed = _parse_hex(args.seed, 32, "seed")
         if seed == bytes(32):
             raise ValueError("all-zero master seed rejected")
-        keys, ivs10 = gen.derive_material(seed, 0, args.lanes, algo_tag=2)
-        ivs = np.ascontiguousarray(ivs10[:, :8])
+        keys, ivs = gen.derive_material(seed, 0, args.lanes, algo_tag=2)
     gen.init_material(np.ascontiguousarray(keys), np.ascontiguousarray(ivs))
 
 

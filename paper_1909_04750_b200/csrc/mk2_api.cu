@@ -5,10 +5,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/mk2.h"
 #include "mk2_kernels.cuh"
@@ -26,6 +32,137 @@ thread_local std::string g_create_error;  // text of this thread's last failed m
 // 16x larger (profiles/r01b_probe_e2e_stage.txt).
 constexpr size_t STAGE_BYTES = size_t(32) << 20;
 constexpr size_t ROW_TILE_FACTOR = 16;
+
+// Restores the caller's current device when an entry point returns: a process that drives torch on cuda:0 and
+// an mk2 context on device 1 keeps its own current device.
+struct DeviceGuard {
+    int prev = -1, dev;
+    bool ok = true;
+    explicit DeviceGuard(int device) : dev(device)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
+// ---------------------------------------------------------------------------
+// Host side of PAGEABLE output buffers.  A D2H copy into pageable memory is staged by the driver
+// through its own small pinned buffers on the calling thread (measured on this box: ~10 GB/s against
+// 55 GB/s into pinned memory).  Here the device staging tile is copied into one of two pinned bounce
+// buffers at link speed and a few worker threads move the previous bounce tile into the caller's
+// array meanwhile (a fresh numpy array also takes its first-touch page faults there, in parallel).
+// One job at a time: a 2-D block copy cut into row slices that the workers (and the calling thread)
+// claim from an atomic counter.
+// ---------------------------------------------------------------------------
+class HostCopyPool {
+public:
+    explicit HostCopyPool(int nthreads)
+    {
+        for (int i = 0; i < nthreads; ++i) workers_.emplace_back([this] { run(); });
+    }
+    ~HostCopyPool()
+    {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : workers_) t.join();
+    }
+    int threads() const { return (int)workers_.size() + 1; }
+    // dst[r * dpitch .. + width) = src[r * spitch .. + width) for r < rows; returns when done
+    void copy2d(uint8_t *dst, size_t dpitch, const uint8_t *src, size_t spitch, size_t width, size_t rows)
+    {
+        if (rows == 0 || width == 0) return;
+        if (dpitch == width && spitch == width) {  // contiguous: one long row
+            width *= rows;
+            rows = 1;
+            dpitch = spitch = width;
+        }
+        auto j = std::make_shared<Job>();
+        j->dst = dst; j->src = src; j->dpitch = dpitch; j->spitch = spitch; j->width = width; j->rows = rows;
+        // slices of about 1 MiB: row ranges or, for one long row, byte ranges
+        if (rows == 1) {
+            j->slice = size_t(1) << 20;
+            j->nslices = (width + j->slice - 1) / j->slice;
+        } else {
+            j->slice = std::max<size_t>(1, (size_t(1) << 20) / width);
+            j->nslices = (rows + j->slice - 1) / j->slice;
+        }
+        j->pending = j->nslices;
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            job_ = j;
+            ++generation_;
+        }
+        cv_.notify_all();
+        work(*j);
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [&] { return j->pending == 0; });
+        job_.reset();
+    }
+
+private:
+    // Every job owns its slice counter, so a worker that wakes up late only finds an exhausted job.
+    struct Job {
+        uint8_t *dst = nullptr;
+        const uint8_t *src = nullptr;
+        size_t dpitch = 0, spitch = 0, width = 0, rows = 0, slice = 1, nslices = 0;
+        std::atomic<size_t> next{0};
+        size_t pending = 0;  // guarded by m_
+    };
+    void work(Job &j)
+    {
+        size_t finished = 0;
+        for (;;) {
+            const size_t i = j.next.fetch_add(1, std::memory_order_relaxed);
+            if (i >= j.nslices) break;
+            if (j.rows == 1) {
+                const size_t o = i * j.slice, n = std::min(j.slice, j.width - o);
+                std::memcpy(j.dst + o, j.src + o, n);
+            } else {
+                const size_t r0 = i * j.slice, r1 = std::min(j.rows, r0 + j.slice);
+                for (size_t r = r0; r < r1; ++r) std::memcpy(j.dst + r * j.dpitch, j.src + r * j.spitch, j.width);
+            }
+            ++finished;
+        }
+        if (finished) {
+            std::lock_guard<std::mutex> lk(m_);
+            j.pending -= finished;
+            if (j.pending == 0) done_.notify_all();
+        }
+    }
+    void run()
+    {
+        unsigned long long seen = 0;
+        for (;;) {
+            std::shared_ptr<Job> j;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || generation_ != seen; });
+                if (stop_) return;
+                seen = generation_;
+                j = job_;
+            }
+            if (j) work(*j);
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::shared_ptr<Job> job_;
+    unsigned long long generation_ = 0;
+    bool stop_ = false;
+};
 }  // namespace
 
 struct mk2_ctx {
@@ -56,6 +193,10 @@ struct mk2_ctx {
     unsigned max_grid = 0;               // debug knob: cap on persistent CTAs (0 = one per SM slot)
     void *d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
+    void *h_bounce[2] = {nullptr, nullptr};  // pinned bounce buffers for PAGEABLE host outputs (one per staging tile)
+    size_t bounce_bytes = 0;
+    HostCopyPool *copy_pool = nullptr;       // worker threads that move bounce tiles into pageable memory (lazy)
+    int host_threads = 0;                    // 0 = automatic
     bool ready = false, async = false, timing_open = false;
     int cipher = 0;        // 0 = MICKEY 2.0, 1 = Grain v1 (which kernels the state belongs to)
     bool row_lsb = false;  // Grain row-major byte packing of the current call
@@ -77,20 +218,49 @@ int fail(mk2_ctx *c, int code, const std::string &msg)
 #define CK(call)                                                                                   \
     do {                                                                                           \
         cudaError_t e_ = (call);                                                                   \
-        if (e_ != cudaSuccess)                                                                     \
+        if (e_ != cudaSuccess) {                                                                   \
+            cudaGetLastError(); /* clear a non-sticky error so that it is not reported twice */    \
             return fail(ctx, e_ == cudaErrorMemoryAllocation ? MK2_E_NOMEM : MK2_E_CUDA,            \
                         std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+        }                                                                                          \
     } while (0)
 
-bool is_device_ptr(const void *p)
+enum class Mem { Device, Pinned, Pageable };
+Mem classify(const void *p)
 {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return Mem::Pageable;
     }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return Mem::Device;
+    return a.type == cudaMemoryTypeHost ? Mem::Pinned : Mem::Pageable;
 }
+bool is_device_ptr(const void *p) { return classify(p) == Mem::Device; }
+
+// Stream-ordered scratch of one call: whatever was allocated is given back to the pool on EVERY exit path
+// (cudaFreeAsync on the launch stream orders the free after the kernels that use it).
+struct Scratch {
+    mk2_ctx *ctx;
+    void *ptr[8] = {};
+    int n = 0;
+    explicit Scratch(mk2_ctx *c) : ctx(c) {}
+    ~Scratch()
+    {
+        for (int i = 0; i < n; ++i)
+            if (ptr[i]) cudaFreeAsync(ptr[i], ctx->stream);
+    }
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    int alloc(void **out, size_t bytes)
+    {
+        *out = nullptr;
+        if (n == 8) return fail(ctx, MK2_E_ARG, "internal: scratch list full");
+        CK(cudaMallocFromPoolAsync(out, bytes, ctx->pool, ctx->stream));
+        ptr[n++] = *out;
+        return MK2_OK;
+    }
+};
 
 inline unsigned blocks_for(uint64_t G, int block = BLOCK) { return (unsigned)((G + block - 1) / block); }
 
@@ -116,6 +286,9 @@ int end_timing(mk2_ctx *ctx)
 int ensure_capacity(mk2_ctx *ctx, uint64_t G)
 {
     if (G <= ctx->cap) return MK2_OK;
+    // whatever happens below, the old state is gone: no later call may launch on freed (or null) buffers
+    ctx->ready = false;
+    ctx->N = ctx->G = 0;
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->d_state) cudaFree(ctx->d_state);
     if (ctx->d_acc) cudaFree(ctx->d_acc);
@@ -155,10 +328,33 @@ int ensure_stage(mk2_ctx *ctx, size_t bytes)
     return MK2_OK;
 }
 
-// Bring a host-or-device input array onto the device (stream ordered).
-int stage_input(mk2_ctx *ctx, const void *src, size_t bytes, const uint8_t **dev, void **owned)
+// Pinned bounce buffers + copy workers for pageable host outputs (see HostCopyPool).
+int ensure_bounce(mk2_ctx *ctx, size_t bytes)
 {
-    *owned = nullptr;
+    if (!ctx->copy_pool) {
+        int n = ctx->host_threads;
+        if (n <= 0) {
+            const unsigned hw = std::thread::hardware_concurrency();
+            n = (int)std::min<unsigned>(8u, std::max<unsigned>(2u, hw / 2));
+        }
+        ctx->copy_pool = new (std::nothrow) HostCopyPool(n - 1);  // the calling thread is the n-th worker
+        if (!ctx->copy_pool) return fail(ctx, MK2_E_NOMEM, "out of host memory");
+    }
+    if (bytes <= ctx->bounce_bytes) return MK2_OK;
+    CK(cudaStreamSynchronize(ctx->copy));
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->h_bounce[b]) cudaFreeHost(ctx->h_bounce[b]);
+        ctx->h_bounce[b] = nullptr;
+    }
+    ctx->bounce_bytes = 0;
+    for (int b = 0; b < 2; ++b) CK(cudaHostAlloc(&ctx->h_bounce[b], bytes, cudaHostAllocDefault));
+    ctx->bounce_bytes = bytes;
+    return MK2_OK;
+}
+
+// Bring a host-or-device input array onto the device (stream ordered).
+int stage_input(mk2_ctx *ctx, Scratch &scratch, const void *src, size_t bytes, const uint8_t **dev)
+{
     if (bytes == 0 || src == nullptr) {
         *dev = nullptr;
         return MK2_OK;
@@ -167,9 +363,11 @@ int stage_input(mk2_ctx *ctx, const void *src, size_t bytes, const uint8_t **dev
         *dev = static_cast<const uint8_t *>(src);
         return MK2_OK;
     }
-    CK(cudaMallocFromPoolAsync(owned, bytes, ctx->pool, ctx->stream));
-    CK(cudaMemcpyAsync(*owned, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    *dev = static_cast<const uint8_t *>(*owned);
+    void *owned = nullptr;
+    int rc = scratch.alloc(&owned, bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(owned, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *dev = static_cast<const uint8_t *>(owned);
     return MK2_OK;
 }
 
@@ -308,10 +506,15 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     // parameter so that every smem offset in the drain loops is an immediate
     const int ts = p.tg == 32 ? (p.block <= 128 ? 128 : p.block <= 192 ? 192 : 224) : 256;
     const size_t smem = (size_t)row_smem_bytes(p.tg, ts);
-#define MK2_ROW_LAUNCH(AL, TGV, TSV)                                                                         \
-    gen_rowmajor_kernel<AL, TGV, TSV><<<p.grid, p.block, smem, ctx->stream>>>(                              \
+#define MK2_ROW_LAUNCH1(AL, TGV, TSV, LSBV)                                                                  \
+    gen_rowmajor_kernel<AL, TGV, TSV, LSBV><<<p.grid, p.block, smem, ctx->stream>>>(                        \
         ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,  \
         ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base)
+#define MK2_ROW_LAUNCH(AL, TGV, TSV)                          \
+    do {                                                      \
+        if (ctx->row_lsb) MK2_ROW_LAUNCH1(AL, TGV, TSV, true); \
+        else MK2_ROW_LAUNCH1(AL, TGV, TSV, false);            \
+    } while (0)
 #define MK2_GRAIN_ROW_LAUNCH(AL, TGV, TSV, LSBV)                                                              \
     grain::gen_rowmajor_kernel<AL, TGV, TSV, LSBV><<<p.grid, p.block, smem, ctx->stream>>>(                  \
         ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,  \
@@ -323,15 +526,15 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
         else if (ctx->row_lsb) MK2_GRAIN_ROW_LAUNCH(false, TGV, TSV, true);            \
         else MK2_GRAIN_ROW_LAUNCH(false, TGV, TSV, false);                             \
     } while (0)
+#define MK2_TMEM_ROW_LAUNCH(AL, LSBV)                                                                        \
+    tmem::gen_rowmajor_kernel<AL, LSBV><<<p.grid, p.block, 0, ctx->stream>>>(                                \
+        ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,  \
+        ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base)
     if (p.tmem) {
-        if (aligned)
-            tmem::gen_rowmajor_kernel<true><<<p.grid, p.block, 0, ctx->stream>>>(
-                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
-                ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
-        else
-            tmem::gen_rowmajor_kernel<false><<<p.grid, p.block, 0, ctx->stream>>>(
-                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc,
-                ctx->d_queue, ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+        if (aligned && ctx->row_lsb) MK2_TMEM_ROW_LAUNCH(true, true);
+        else if (aligned) MK2_TMEM_ROW_LAUNCH(true, false);
+        else if (ctx->row_lsb) MK2_TMEM_ROW_LAUNCH(false, true);
+        else MK2_TMEM_ROW_LAUNCH(false, false);
     } else if (ctx->cipher == 1) {
         if (ts == 128) MK2_GRAIN_ROW_PICK(32, 128);
         else if (ts == 192) MK2_GRAIN_ROW_PICK(32, 192);
@@ -346,7 +549,9 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     } else {
         if (aligned) MK2_ROW_LAUNCH(true, 16, 256); else MK2_ROW_LAUNCH(false, 16, 256);
     }
+#undef MK2_TMEM_ROW_LAUNCH
 #undef MK2_ROW_LAUNCH
+#undef MK2_ROW_LAUNCH1
 #undef MK2_GRAIN_ROW_PICK
 #undef MK2_GRAIN_ROW_LAUNCH
     CK(cudaGetLastError());
@@ -371,19 +576,135 @@ int drain_copies(mk2_ctx *ctx)
     return MK2_OK;
 }
 
+// D2H side of a host-output call.  Tile i is generated into device staging buffer b = i & 1 (caller:
+// acquire_stage + launch), then copy_out() moves it to the caller's array:
+//   pinned destination   -> one async (2-D) copy on the copy stream, straight into the array;
+//   pageable destination -> async copy into pinned bounce buffer b at link speed; the calling thread and the
+//                           copy workers move bounce tile i-1 into the array while tile i crosses the link
+//                           and tile i+1 is generated.
+// finish() waits for everything (the API returns with the array complete).
+class HostTiles {
+public:
+    HostTiles(mk2_ctx *c, bool pageable) : ctx(c), bounce(pageable) {}
+    bool pageable() const { return bounce; }
+    int prepare(size_t tile_bytes) { return bounce ? ensure_bounce(ctx, tile_bytes) : MK2_OK; }
+    int next() { return (int)(count++ & 1); }
+    // rows x width bytes from staging buffer b (pitch spitch) to dst (pitch dpitch)
+    int copy_out(int b, uint8_t *dst, size_t dpitch, size_t spitch, size_t width, size_t rows)
+    {
+        CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
+        if (!bounce) {
+            if (dpitch == width && spitch == width)
+                CK(cudaMemcpyAsync(dst, ctx->d_stage[b], width * rows, cudaMemcpyDeviceToHost, ctx->copy));
+            else
+                CK(cudaMemcpy2DAsync(dst, dpitch, ctx->d_stage[b], spitch, width, rows, cudaMemcpyDeviceToHost, ctx->copy));
+        } else {
+            // bounce buffer b still holds tile i-2 until the workers have moved it out: flush it first
+            int rc = flush(b);
+            if (rc) return rc;
+            if (spitch == width)
+                CK(cudaMemcpyAsync(ctx->h_bounce[b], ctx->d_stage[b], width * rows, cudaMemcpyDeviceToHost, ctx->copy));
+            else
+                CK(cudaMemcpy2DAsync(ctx->h_bounce[b], width, ctx->d_stage[b], spitch, width, rows, cudaMemcpyDeviceToHost,
+                                     ctx->copy));
+            pend[b] = {dst, dpitch, width, rows, true};
+        }
+        CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
+        ctx->copy_pending[b] = true;
+        if (bounce) {  // move the PREVIOUS tile out while this one is in flight
+            int rc = flush(b ^ 1);
+            if (rc) return rc;
+        }
+        return MK2_OK;
+    }
+    int finish()
+    {
+        if (bounce) {
+            int rc;
+            const int last = (int)((count + 1) & 1);  // older tile first
+            if ((rc = flush(last ^ 1)) || (rc = flush(last))) return rc;
+        }
+        return drain_copies(ctx);
+    }
+
+private:
+    struct Pending {
+        uint8_t *dst = nullptr;
+        size_t dpitch = 0, width = 0, rows = 0;
+        bool live = false;
+    };
+    int flush(int b)
+    {
+        if (!pend[b].live) return MK2_OK;
+        CK(cudaEventSynchronize(ctx->copy_done[b]));
+        ctx->copy_pool->copy2d(pend[b].dst, pend[b].dpitch, static_cast<const uint8_t *>(ctx->h_bounce[b]), pend[b].width,
+                               pend[b].width, pend[b].rows);
+        pend[b].live = false;
+        return MK2_OK;
+    }
+    mk2_ctx *ctx;
+    bool bounce;
+    uint64_t count = 0;
+    Pending pend[2];
+};
+
 int check_ready(mk2_ctx *ctx)
 {
     if (!ctx) return MK2_E_ARG;
-    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MK2_E_CUDA, "cudaSetDevice failed");
     if (!ctx->ready) return fail(ctx, MK2_E_STATE, "context holds no key/IV material: call mk2_init_* first");
     return MK2_OK;
+}
+
+// Every entry point that touches CUDA: NULL check, then run on the context's device and put the caller's
+// current device back on return.
+#define MK2_ENTER(c)                                                                   \
+    if (!(c)) return MK2_E_ARG;                                                        \
+    DeviceGuard device_guard_((c)->device);                                            \
+    if (!device_guard_.ok) return fail((c), MK2_E_CUDA, "cudaSetDevice failed")
+
+// Opt-in to > 48 KiB of dynamic shared memory for the shared-memory row-major kernels: a per-device function
+// attribute, set once per process and device instead of 24 cudaFuncSetAttribute calls per context.
+cudaError_t opt_in_row_kernels(int device)
+{
+    static std::mutex m;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lk(m);
+    if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    const int row_smem_max = row_smem_bytes(32, 224);  // the largest staging tile: 224 KiB
+    auto opt_in = [&](auto kernel) {
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, row_smem_max);
+    };
+#define MK2_OPT_IN_MICKEY(TGV, TSV)                          \
+    opt_in(gen_rowmajor_kernel<true, TGV, TSV, true>);       \
+    opt_in(gen_rowmajor_kernel<true, TGV, TSV, false>);      \
+    opt_in(gen_rowmajor_kernel<false, TGV, TSV, true>);      \
+    opt_in(gen_rowmajor_kernel<false, TGV, TSV, false>)
+    MK2_OPT_IN_MICKEY(32, 128);
+    MK2_OPT_IN_MICKEY(32, 192);
+    MK2_OPT_IN_MICKEY(32, 224);
+    MK2_OPT_IN_MICKEY(16, 256);
+#undef MK2_OPT_IN_MICKEY
+#define MK2_OPT_IN_GRAIN(TGV, TSV)                                  \
+    opt_in(grain::gen_rowmajor_kernel<true, TGV, TSV, true>);       \
+    opt_in(grain::gen_rowmajor_kernel<true, TGV, TSV, false>);      \
+    opt_in(grain::gen_rowmajor_kernel<false, TGV, TSV, true>);      \
+    opt_in(grain::gen_rowmajor_kernel<false, TGV, TSV, false>)
+    MK2_OPT_IN_GRAIN(32, 128);
+    MK2_OPT_IN_GRAIN(32, 192);
+    MK2_OPT_IN_GRAIN(32, 224);
+    MK2_OPT_IN_GRAIN(16, 256);
+#undef MK2_OPT_IN_GRAIN
+    if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
+    return e;
 }
 
 }  // namespace
 
 extern "C" {
 
-int mk2_abi_version(void) { return 1; }
+int mk2_abi_version(void) { return 2; }
 
 int mk2_lop3_per_clock(void) { return 327; }
 static int rblock_of(int kernel)
@@ -424,7 +745,8 @@ int mk2_create(int device, mk2_ctx **out)
         return fail(nullptr, MK2_E_NODEVICE,
                     std::string("device is sm_") + std::to_string(prop.major) + std::to_string(prop.minor) +
                         "; the kernels are built for sm_100a only");
-    CK(cudaSetDevice(device));
+    DeviceGuard guard(device);
+    if (!guard.ok) return fail(nullptr, MK2_E_CUDA, "cudaSetDevice failed");
     mk2_ctx *c = new (std::nothrow) mk2_ctx();
     if (!c) return fail(nullptr, MK2_E_NOMEM, "out of host memory");
     c->device = device;
@@ -453,28 +775,7 @@ int mk2_create(int device, mk2_ctx **out)
     }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_sum, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_queue, sizeof(SchedQueue));
-    const int row_smem_max = row_smem_bytes(32, 224);  // the largest staging tile: 224 KiB
-    auto opt_in = [&](auto kernel) {
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, row_smem_max);
-    };
-    opt_in(gen_rowmajor_kernel<true, 32, 128>);
-    opt_in(gen_rowmajor_kernel<false, 32, 128>);
-    opt_in(gen_rowmajor_kernel<true, 32, 192>);
-    opt_in(gen_rowmajor_kernel<false, 32, 192>);
-    opt_in(gen_rowmajor_kernel<true, 32, 224>);
-    opt_in(gen_rowmajor_kernel<false, 32, 224>);
-    opt_in(gen_rowmajor_kernel<true, 16, 256>);
-    opt_in(gen_rowmajor_kernel<false, 16, 256>);
-#define MK2_OPT_IN_GRAIN(TGV, TSV)                                  \
-    opt_in(grain::gen_rowmajor_kernel<true, TGV, TSV, true>);       \
-    opt_in(grain::gen_rowmajor_kernel<true, TGV, TSV, false>);      \
-    opt_in(grain::gen_rowmajor_kernel<false, TGV, TSV, true>);      \
-    opt_in(grain::gen_rowmajor_kernel<false, TGV, TSV, false>)
-    MK2_OPT_IN_GRAIN(32, 128);
-    MK2_OPT_IN_GRAIN(32, 192);
-    MK2_OPT_IN_GRAIN(32, 224);
-    MK2_OPT_IN_GRAIN(16, 256);
-#undef MK2_OPT_IN_GRAIN
+    if (e == cudaSuccess) e = opt_in_row_kernels(device);
     if (e != cudaSuccess) {
         std::string msg = std::string("context setup: ") + cudaGetErrorString(e);
         mk2_destroy(c);
@@ -488,7 +789,9 @@ int mk2_create(int device, mk2_ctx **out)
 int mk2_destroy(mk2_ctx *ctx)
 {
     if (!ctx) return MK2_OK;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
+    delete ctx->copy_pool;
+    ctx->copy_pool = nullptr;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->copy) cudaStreamSynchronize(ctx->copy);
     if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
@@ -497,6 +800,7 @@ int mk2_destroy(mk2_ctx *ctx)
         if (ctx->h2d_done[b]) cudaEventDestroy(ctx->h2d_done[b]);
         if (ctx->mat_used[b]) cudaEventDestroy(ctx->mat_used[b]);
         if (ctx->d_stage[b]) cudaFree(ctx->d_stage[b]);
+        if (ctx->h_bounce[b]) cudaFreeHost(ctx->h_bounce[b]);
         if (ctx->gen_done[b]) cudaEventDestroy(ctx->gen_done[b]);
         if (ctx->copy_done[b]) cudaEventDestroy(ctx->copy_done[b]);
     }
@@ -520,8 +824,7 @@ int mk2_destroy(mk2_ctx *ctx)
 
 int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream)
 {
-    if (!ctx) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->stream = static_cast<cudaStream_t>(cuda_stream);  // 0 is a real stream: the legacy default stream
     return MK2_OK;
@@ -529,8 +832,7 @@ int mk2_set_stream(mk2_ctx *ctx, void *cuda_stream)
 
 int mk2_use_own_stream(mk2_ctx *ctx)
 {
-    if (!ctx) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->stream = ctx->own;
     return MK2_OK;
@@ -538,8 +840,7 @@ int mk2_use_own_stream(mk2_ctx *ctx)
 
 int mk2_set_trace(mk2_ctx *ctx, uint64_t capacity)
 {
-    if (!ctx) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->trace.rec) cudaFree(ctx->trace.rec);
     if (ctx->trace.count) cudaFree(ctx->trace.count);
@@ -558,7 +859,7 @@ int mk2_read_trace(mk2_ctx *ctx, void *records, uint64_t max_records, uint64_t *
     if (!ctx || !count) return MK2_E_ARG;
     *count = 0;
     if (!ctx->trace.rec) return MK2_OK;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     unsigned long long n = 0;
     CK(cudaMemcpy(&n, ctx->trace.count, sizeof n, cudaMemcpyDeviceToHost));
@@ -620,6 +921,43 @@ int mk2_set_block_threads(mk2_ctx *ctx, int threads)
     return MK2_OK;
 }
 
+int mk2_set_host_threads(mk2_ctx *ctx, int threads)
+{
+    if (!ctx) return MK2_E_ARG;
+    if (threads < 0 || threads > 256) return fail(ctx, MK2_E_ARG, "host threads must be 0 (automatic) or 1..256");
+    if (threads != ctx->host_threads) {
+        delete ctx->copy_pool;  // idle between calls; re-created with the new size on next use
+        ctx->copy_pool = nullptr;
+        ctx->host_threads = threads;
+    }
+    return MK2_OK;
+}
+
+int mk2_host_alloc(size_t bytes, void **out)
+{
+    if (!out) return MK2_E_ARG;
+    *out = nullptr;
+    if (bytes == 0) return MK2_OK;
+    const cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(nullptr, e == cudaErrorMemoryAllocation ? MK2_E_NOMEM : MK2_E_CUDA,
+                    std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    }
+    return MK2_OK;
+}
+
+int mk2_host_free(void *p)
+{
+    if (!p) return MK2_OK;
+    if (cudaFreeHost(p) != cudaSuccess) {
+        cudaGetLastError();
+        return MK2_E_CUDA;
+    }
+    return MK2_OK;
+}
+
 int mk2_set_async(mk2_ctx *ctx, int async)
 {
     if (!ctx) return MK2_E_ARG;
@@ -629,8 +967,7 @@ int mk2_set_async(mk2_ctx *ctx, int async)
 
 int mk2_trim(mk2_ctx *ctx)
 {
-    if (!ctx) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaStreamSynchronize(ctx->copy));
     for (int b = 0; b < 2; ++b) {
@@ -645,8 +982,7 @@ int mk2_trim(mk2_ctx *ctx)
 
 int mk2_sync(mk2_ctx *ctx)
 {
-    if (!ctx) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaStreamSynchronize(ctx->copy));
     if (ctx->timing_open) {
@@ -679,15 +1015,13 @@ int mk2_last_kernel_launches(const mk2_ctx *ctx) { return ctx ? ctx->last_launch
 
 static int init_common(mk2_ctx *ctx, uint64_t N)
 {
-    if (!ctx) return MK2_E_ARG;
     if (N == 0) return fail(ctx, MK2_E_ARG, "at least one lane is required");
-    CK(cudaSetDevice(ctx->device));
     const uint64_t G = (N + 31) / 32;
+    ctx->ready = false;  // whatever happens from here on, the previous state is no longer valid
     int rc = ensure_capacity(ctx, G);
     if (rc) return rc;
     ctx->N = N;
     ctx->G = G;
-    ctx->ready = false;
     return MK2_OK;
 }
 
@@ -695,45 +1029,44 @@ static int init_common(mk2_ctx *ctx, uint64_t N)
 static int init_uniform_device(mk2_ctx *ctx, const uint8_t *dk, const uint8_t *di, uint32_t iv_stride, uint32_t iv_bits)
 {
     int rc;
-    uint32_t *mat = nullptr;
+    Scratch scratch(ctx);
+    void *matp = nullptr;
     const int load = (int)iv_bits + KEY_BITS;
-    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)load * ctx->G, ctx->pool, ctx->stream));
+    if ((rc = scratch.alloc(&matp, sizeof(uint32_t) * (size_t)load * ctx->G))) return rc;
+    uint32_t *mat = static_cast<uint32_t *>(matp);
     const bool fast10 = reinterpret_cast<uintptr_t>(dk) % 16 == 0 &&
                         (!iv_bits || (iv_stride == 10 && reinterpret_cast<uintptr_t>(di) % 16 == 0));
     pack_uniform_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, (int)iv_bits, ctx->N, ctx->G, mat,
                                                                         fast10);
     CK(cudaGetLastError());
     ctx->last_launches++;
-    if ((rc = launch_init(ctx, mat, load, 0, false))) return rc;
-    CK(cudaFreeAsync(mat, ctx->stream));
-    return MK2_OK;
+    return launch_init(ctx, mat, load, 0, false);
 }
 
 int mk2_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
                            uint32_t iv_bits, uint64_t N)
 {
-    int rc = init_common(ctx, N);
-    if (rc) return rc;
+    MK2_ENTER(ctx);
     if (!keys) return fail(ctx, MK2_E_ARG, "keys is NULL");
     if (iv_bits > 80) return fail(ctx, MK2_E_ARG, "IV must be at most 80 bits");
     if (iv_bits && (!ivs || iv_stride < (iv_bits + 7) / 8)) return fail(ctx, MK2_E_ARG, "ivs/iv_stride too small for iv_bits");
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
     if ((rc = begin_timing(ctx))) return rc;
+    Scratch scratch(ctx);
     const uint8_t *dk = nullptr, *di = nullptr;
-    void *ok = nullptr, *oi = nullptr;
-    if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
-    if ((rc = stage_input(ctx, iv_bits ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
+    if ((rc = stage_input(ctx, scratch, keys, N * 10, &dk))) return rc;
+    if ((rc = stage_input(ctx, scratch, iv_bits ? ivs : nullptr, N * (size_t)iv_stride, &di))) return rc;
     if ((rc = init_uniform_device(ctx, dk, di, iv_stride, iv_bits))) return rc;
-    if (ok) CK(cudaFreeAsync(ok, ctx->stream));
-    if (oi) CK(cudaFreeAsync(oi, ctx->stream));
     return end_timing(ctx);
 }
 
 int mk2_init_ragged(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride,
                     const uint8_t *iv_nbits, uint64_t N)
 {
-    int rc = init_common(ctx, N);
-    if (rc) return rc;
+    MK2_ENTER(ctx);
     if (!keys || !iv_nbits) return fail(ctx, MK2_E_ARG, "keys / iv_nbits is NULL");
+    if (N == 0) return fail(ctx, MK2_E_ARG, "at least one lane is required");
     // the lengths steer the launch, so they are needed on the host
     std::string lens(N, '\0');
     if (is_device_ptr(iv_nbits)) {
@@ -750,92 +1083,105 @@ int mk2_init_ragged(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint3
         lmax = std::max(lmax, (int)l);
     }
     if (lmax && (!ivs || iv_stride < (uint32_t)(lmax + 7) / 8)) return fail(ctx, MK2_E_ARG, "ivs/iv_stride too small");
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
     if ((rc = begin_timing(ctx))) return rc;
+    Scratch scratch(ctx);
     const uint8_t *dk = nullptr, *di = nullptr, *dn = nullptr;
-    void *ok = nullptr, *oi = nullptr, *on = nullptr;
-    uint32_t *mat = nullptr;
-    if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
-    if ((rc = stage_input(ctx, lmax ? ivs : nullptr, N * (size_t)iv_stride, &di, &oi))) return rc;
-    if ((rc = stage_input(ctx, iv_nbits, N, &dn, &on))) return rc;
+    void *matp = nullptr;
+    if ((rc = stage_input(ctx, scratch, keys, N * 10, &dk))) return rc;
+    if ((rc = stage_input(ctx, scratch, lmax ? ivs : nullptr, N * (size_t)iv_stride, &di))) return rc;
+    if ((rc = stage_input(ctx, scratch, iv_nbits, N, &dn))) return rc;
     const int load = lmax + KEY_BITS;
-    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)(2 * lmax + KEY_BITS + 1) * ctx->G, ctx->pool, ctx->stream));
-    pack_ragged_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, dn, lmax, N, ctx->G, mat);
+    if ((rc = scratch.alloc(&matp, sizeof(uint32_t) * (size_t)(2 * lmax + KEY_BITS + 1) * ctx->G))) return rc;
+    uint32_t *mat = static_cast<uint32_t *>(matp);
+    auto al16 = [](const void *q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+    const bool fast10 = al16(dk) && al16(dn) && (!lmax || (iv_stride == 10 && al16(di)));
+    pack_ragged_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(dk, di, iv_stride, dn, lmax, N, ctx->G, mat, fast10);
     CK(cudaGetLastError());
     ctx->last_launches++;
     if ((rc = launch_init(ctx, mat, load, lmax, true))) return rc;
-    CK(cudaFreeAsync(mat, ctx->stream));
-    if (ok) CK(cudaFreeAsync(ok, ctx->stream));
-    if (oi) CK(cudaFreeAsync(oi, ctx->stream));
-    if (on) CK(cudaFreeAsync(on, ctx->stream));
     return end_timing(ctx);
 }
 
 int mk2_init_counter_iv(mk2_ctx *ctx, const uint8_t key[10], uint64_t first_index, uint64_t N)
 {
-    int rc = init_common(ctx, N);
-    if (rc) return rc;
+    MK2_ENTER(ctx);
     if (!key) return fail(ctx, MK2_E_ARG, "key is NULL");
     if (first_index % 32) return fail(ctx, MK2_E_ARG, "first_index must be a multiple of 32");
     if (first_index + N < first_index) return fail(ctx, MK2_E_ARG, "instance index range overflows 64 bits");
+    int rc = init_common(ctx, N);
+    if (rc) return rc;
     uint64_t hi = ((uint64_t)key[0] << 8) | key[1], lo = 0;
     for (int i = 2; i < 10; ++i) lo = (lo << 8) | key[i];
     if ((rc = begin_timing(ctx))) return rc;
-    uint32_t *mat = nullptr;
-    CK(cudaMallocFromPoolAsync(&mat, sizeof(uint32_t) * (size_t)160 * ctx->G, ctx->pool, ctx->stream));
+    Scratch scratch(ctx);
+    void *matp = nullptr;
+    if ((rc = scratch.alloc(&matp, sizeof(uint32_t) * (size_t)160 * ctx->G))) return rc;
+    uint32_t *mat = static_cast<uint32_t *>(matp);
     pack_counter_kernel<<<blocks_for(ctx->G), BLOCK, 0, ctx->stream>>>(hi, lo, first_index, ctx->G, mat);
     CK(cudaGetLastError());
     ctx->last_launches++;
     if ((rc = launch_init(ctx, mat, 160, 0, false))) return rc;
-    CK(cudaFreeAsync(mat, ctx->stream));
     return end_timing(ctx);
 }
 
-// Derive key/IV rows for lanes [first_lane, first_lane + N) into device buffers (stream ordered).
-static int derive_to_device(mk2_ctx *ctx, const uint8_t seed[32], uint32_t tag, uint64_t first_lane, uint64_t N,
-                            uint8_t *d_keys, uint8_t *d_ivs)
+// IV bytes per lane of a derivation tag (seedgen.py:24-31, _SIZES / _ALGO_TAGS): 2 = grain (10 + 8),
+// 3 = mickey (10 + 10).  Tag 1 (aes-ctr: 16-byte key + 12-byte nonce) is not on this library's path.
+static int derive_iv_len(uint32_t tag) { return tag == 3u ? 10 : tag == 2u ? 8 : 0; }
+
+static int derive_check(mk2_ctx *ctx, const uint8_t seed[32], uint32_t tag, uint64_t first_lane, uint64_t N)
 {
     if (!seed) return fail(ctx, MK2_E_ARG, "seed is NULL");
+    if (!derive_iv_len(tag)) return fail(ctx, MK2_E_ARG, "algo_tag must be 2 (grain) or 3 (mickey)");
     if (N == 0) return fail(ctx, MK2_E_ARG, "at least one lane is required");
     if (first_lane + N > (1ull << 32) || first_lane + N < first_lane)
         return fail(ctx, MK2_E_ARG, "lane index must fit the 32-bit field of the derivation block");
     bool nonzero = false;
     for (int i = 0; i < 32; ++i) nonzero |= seed[i] != 0;
     if (!nonzero) return fail(ctx, MK2_E_ARG, "all-zero master seed rejected");
+    return MK2_OK;
+}
+
+// Derive key/IV rows for lanes [first_lane, first_lane + N) into device buffers (stream ordered); arguments
+// already validated by derive_check.
+static int derive_to_device(mk2_ctx *ctx, Scratch &scratch, const uint8_t seed[32], uint32_t tag, uint64_t first_lane,
+                            uint64_t N, uint8_t *d_keys, uint8_t *d_ivs)
+{
+    int rc;
     void *d_seed = nullptr, *d_rk = nullptr;
-    CK(cudaMallocFromPoolAsync(&d_seed, 32, ctx->pool, ctx->stream));
-    CK(cudaMallocFromPoolAsync(&d_rk, 44 * sizeof(uint32_t), ctx->pool, ctx->stream));
+    if ((rc = scratch.alloc(&d_seed, 32))) return rc;
+    if ((rc = scratch.alloc(&d_rk, 44 * sizeof(uint32_t)))) return rc;
     CK(cudaMemcpyAsync(d_seed, seed, 32, cudaMemcpyHostToDevice, ctx->stream));
     seed_setup_kernel<<<1, 256, 0, ctx->stream>>>(static_cast<const uint8_t *>(d_seed), static_cast<uint32_t *>(d_rk));
     CK(cudaGetLastError());
     // grid-stride kernel: six 256-thread CTAs per SM (32 KB of table each) cover any N
     const unsigned derive_grid = (unsigned)std::min<uint64_t>((N + 255) / 256, 6ull * (uint64_t)ctx->sm_count);
-    seed_derive_kernel<<<derive_grid, 256, 0, ctx->stream>>>(static_cast<const uint32_t *>(d_rk), tag,
-                                                                             first_lane, N, d_keys, d_ivs);
+    seed_derive_kernel<<<derive_grid, 256, 0, ctx->stream>>>(static_cast<const uint32_t *>(d_rk), tag, first_lane, N,
+                                                             derive_iv_len(tag), d_keys, d_ivs);
     CK(cudaGetLastError());
     ctx->last_launches += 2;
-    CK(cudaFreeAsync(d_seed, ctx->stream));
-    CK(cudaFreeAsync(d_rk, ctx->stream));
     return MK2_OK;
 }
 
 int mk2_derive_material(mk2_ctx *ctx, const uint8_t seed[32], uint32_t algo_tag, uint64_t first_lane, uint64_t N,
                         uint8_t *keys, uint8_t *ivs)
 {
-    if (!ctx) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    MK2_ENTER(ctx);
     if (!keys || !ivs) return fail(ctx, MK2_E_ARG, "keys / ivs is NULL");
-    int rc = begin_timing(ctx);
+    int rc = derive_check(ctx, seed, algo_tag, first_lane, N);
     if (rc) return rc;
+    if ((rc = begin_timing(ctx))) return rc;
+    const size_t iv_len = (size_t)derive_iv_len(algo_tag);
     const bool dk = is_device_ptr(keys), di = is_device_ptr(ivs);
+    Scratch scratch(ctx);
     void *tk = nullptr, *ti = nullptr;
-    if (!dk) CK(cudaMallocFromPoolAsync(&tk, N * 10, ctx->pool, ctx->stream));
-    if (!di) CK(cudaMallocFromPoolAsync(&ti, N * 10, ctx->pool, ctx->stream));
+    if (!dk && (rc = scratch.alloc(&tk, N * 10))) return rc;
+    if (!di && (rc = scratch.alloc(&ti, N * iv_len))) return rc;
     uint8_t *pk = dk ? keys : static_cast<uint8_t *>(tk), *pi = di ? ivs : static_cast<uint8_t *>(ti);
-    if ((rc = derive_to_device(ctx, seed, algo_tag, first_lane, N, pk, pi))) return rc;
+    if ((rc = derive_to_device(ctx, scratch, seed, algo_tag, first_lane, N, pk, pi))) return rc;
     if (!dk) CK(cudaMemcpyAsync(keys, tk, N * 10, cudaMemcpyDeviceToHost, ctx->stream));
-    if (!di) CK(cudaMemcpyAsync(ivs, ti, N * 10, cudaMemcpyDeviceToHost, ctx->stream));
-    if (tk) CK(cudaFreeAsync(tk, ctx->stream));
-    if (ti) CK(cudaFreeAsync(ti, ctx->stream));
+    if (!di) CK(cudaMemcpyAsync(ivs, ti, N * iv_len, cudaMemcpyDeviceToHost, ctx->stream));
     if ((rc = end_timing(ctx))) return rc;
     if (!dk || !di) CK(cudaStreamSynchronize(ctx->stream));
     return MK2_OK;
@@ -843,18 +1189,18 @@ int mk2_derive_material(mk2_ctx *ctx, const uint8_t seed[32], uint32_t algo_tag,
 
 int mk2_init_from_seed(mk2_ctx *ctx, const uint8_t seed[32], uint64_t first_lane, uint64_t N)
 {
-    int rc = init_common(ctx, N);
+    MK2_ENTER(ctx);
+    int rc = derive_check(ctx, seed, 3u /* mickey */, first_lane, N);
     if (rc) return rc;
+    if ((rc = init_common(ctx, N))) return rc;
     if ((rc = begin_timing(ctx))) return rc;
+    Scratch scratch(ctx);
     void *dk = nullptr, *di = nullptr;
-    CK(cudaMallocFromPoolAsync(&dk, N * 10, ctx->pool, ctx->stream));
-    CK(cudaMallocFromPoolAsync(&di, N * 10, ctx->pool, ctx->stream));
-    if ((rc = derive_to_device(ctx, seed, 3u /* mickey */, first_lane, N, static_cast<uint8_t *>(dk),
-                               static_cast<uint8_t *>(di))))
+    if ((rc = scratch.alloc(&dk, N * 10))) return rc;
+    if ((rc = scratch.alloc(&di, N * 10))) return rc;
+    if ((rc = derive_to_device(ctx, scratch, seed, 3u, first_lane, N, static_cast<uint8_t *>(dk), static_cast<uint8_t *>(di))))
         return rc;
     if ((rc = init_uniform_device(ctx, static_cast<const uint8_t *>(dk), static_cast<const uint8_t *>(di), 10, 80))) return rc;
-    CK(cudaFreeAsync(dk, ctx->stream));
-    CK(cudaFreeAsync(di, ctx->stream));
     return end_timing(ctx);
 }
 
@@ -873,26 +1219,36 @@ static int check_cipher(mk2_ctx *ctx, int cipher)
 
 int mk2_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words)
 {
+    MK2_ENTER(ctx);
     int rc = check_cipher(ctx, 0);
     return rc ? rc : generate_colmajor_impl(ctx, T, out, stride_words);
 }
 
 int mk2_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes)
 {
+    return mk2_generate_rowmajor_order(ctx, T, out, pitch_bytes, 0);
+}
+
+int mk2_generate_rowmajor_order(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes, int lsb_first)
+{
+    MK2_ENTER(ctx);
     int rc = check_cipher(ctx, 0);
-    return rc ? rc : generate_rowmajor_impl(ctx, T, out, pitch_bytes);
+    if (rc) return rc;
+    ctx->row_lsb = lsb_first != 0;
+    return generate_rowmajor_impl(ctx, T, out, pitch_bytes);
 }
 
 int mk2_grain_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint64_t N)
 {
+    MK2_ENTER(ctx);
+    if (!keys || !ivs) return fail(ctx, MK2_E_ARG, "keys / ivs is NULL");
     int rc = init_common(ctx, N);
     if (rc) return rc;
-    if (!keys || !ivs) return fail(ctx, MK2_E_ARG, "keys / ivs is NULL");
     if ((rc = begin_timing(ctx))) return rc;
+    Scratch scratch(ctx);
     const uint8_t *dk = nullptr, *di = nullptr;
-    void *ok = nullptr, *oi = nullptr;
-    if ((rc = stage_input(ctx, keys, N * 10, &dk, &ok))) return rc;
-    if ((rc = stage_input(ctx, ivs, N * 8, &di, &oi))) return rc;
+    if ((rc = stage_input(ctx, scratch, keys, N * 10, &dk))) return rc;
+    if ((rc = stage_input(ctx, scratch, ivs, N * 8, &di))) return rc;
     grain::init_kernel<<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(dk, di, N, ctx->G, ctx->d_state,
                                                                                         ctx->d_acc);
     CK(cudaGetLastError());
@@ -900,19 +1256,19 @@ int mk2_grain_init_from_material(mk2_ctx *ctx, const uint8_t *keys, const uint8_
     ctx->clocks = 0;
     ctx->cipher = 1;
     ctx->ready = true;
-    if (ok) CK(cudaFreeAsync(ok, ctx->stream));
-    if (oi) CK(cudaFreeAsync(oi, ctx->stream));
     return end_timing(ctx);
 }
 
 int mk2_grain_generate_colmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t stride_words)
 {
+    MK2_ENTER(ctx);
     int rc = check_cipher(ctx, 1);
     return rc ? rc : generate_colmajor_impl(ctx, T, out, stride_words);
 }
 
 int mk2_grain_generate_rowmajor(mk2_ctx *ctx, uint64_t T, void *out, uint64_t pitch_bytes, int lsb_first)
 {
+    MK2_ENTER(ctx);
     int rc = check_cipher(ctx, 1);
     if (rc) return rc;
     ctx->row_lsb = lsb_first != 0;
@@ -933,30 +1289,28 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
     if (stride_words >= (1ull << 30)) return fail(ctx, MK2_E_ARG, "stride_words must be below 2^30");  // 32-bit byte strides in the kernels
     if (reinterpret_cast<uintptr_t>(out) % 4) return fail(ctx, MK2_E_ARG, "out must be 4-byte aligned");
     if ((rc = begin_timing(ctx))) return rc;
-    if (is_device_ptr(out)) {
+    const Mem mem = classify(out);
+    if (mem == Mem::Device) {
         if ((rc = launch_col(ctx, T, static_cast<uint32_t *>(out), stride_words))) return rc;
     } else {
+        // Host output: keystream tiles are produced in two device staging buffers and copied out on a second
+        // stream while the next tile is generated.  Pinned destinations take the D2H copy directly; pageable
+        // ones go through the pinned bounce buffers and the copy workers (HostTiles).
         const size_t row_bytes = ctx->G * sizeof(uint32_t);
         const size_t want = std::max<size_t>(std::min<size_t>(ctx->stage_target, T * row_bytes), row_bytes);
         if ((rc = ensure_stage(ctx, want))) return rc;
+        HostTiles tiles(ctx, mem == Mem::Pageable);
+        if ((rc = tiles.prepare(ctx->stage_bytes))) return rc;
         const uint64_t chunk = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
-        int b = 0;
-        for (uint64_t t0 = 0; t0 < T; t0 += chunk, b ^= 1) {
+        for (uint64_t t0 = 0; t0 < T; t0 += chunk) {
             const uint64_t tc = std::min(chunk, T - t0);
+            const int b = tiles.next();
             if ((rc = acquire_stage(ctx, b))) return rc;
             if ((rc = launch_col(ctx, tc, static_cast<uint32_t *>(ctx->d_stage[b]), ctx->G))) return rc;
-            CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
-            CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
             uint8_t *dst = static_cast<uint8_t *>(out) + t0 * stride_words * sizeof(uint32_t);
-            if (stride_words == ctx->G)
-                CK(cudaMemcpyAsync(dst, ctx->d_stage[b], row_bytes * tc, cudaMemcpyDeviceToHost, ctx->copy));
-            else
-                CK(cudaMemcpy2DAsync(dst, stride_words * sizeof(uint32_t), ctx->d_stage[b], row_bytes, row_bytes, tc,
-                                     cudaMemcpyDeviceToHost, ctx->copy));
-            CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
-            ctx->copy_pending[b] = true;
+            if ((rc = tiles.copy_out(b, dst, stride_words * sizeof(uint32_t), row_bytes, row_bytes, tc))) return rc;
         }
-        if ((rc = drain_copies(ctx))) return rc;
+        if ((rc = tiles.finish())) return rc;
     }
     ctx->clocks += T;
     return end_timing(ctx);
@@ -967,41 +1321,36 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
 // drain_copies).  A tile is a contiguous run of instance rows, each >= 512 B wide whenever T allows,
 // so the D2H copy is one wide 2-D (or plain 1-D) transfer; a chain block is large enough to occupy
 // every worker warp.  Chains stay strictly serial in time because the time loop is the inner one.
-static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch_bytes, int &b)
+static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch_bytes, HostTiles &tiles)
 {
     int rc;
     const uint64_t chains = (ctx->G + 31) / 32;
     // tile = [block_chains x 1024 rows] x [tc_max clocks] of about ROW_TILE_FACTOR x stage_target bytes, rows at
     // least 512 B wide when T allows (narrower 2-D copies collapse: 192 B rows 37 GB/s, 64 B rows 16 GB/s), and
     // between one and two chains per worker warp of a full launch
-    const uint64_t tile_bytes = ROW_TILE_FACTOR * ctx->stage_target;
+    // (pageable destinations: a quarter of that, because the last tile's move out of the bounce buffer is exposed
+    // at the end of the call; the link, not the kernel, is the bottleneck, so smaller launches cost nothing)
+    const uint64_t tile_bytes = (tiles.pageable() ? ROW_TILE_FACTOR / 4 : ROW_TILE_FACTOR) * ctx->stage_target;
     const uint64_t min_clocks = std::min<uint64_t>((T + 255) / 256 * 256, 4096);
-    const uint64_t workers = 8ull * (uint64_t)ctx->sm_count;
+    const uint64_t workers = (tiles.pageable() ? 2ull : 8ull) * (uint64_t)ctx->sm_count;
     const uint64_t want_chains = std::min<uint64_t>(2 * workers, std::max<uint64_t>(workers, tile_bytes / (min_clocks / 8) / 1024));
     const uint64_t block_chains = std::min<uint64_t>(chains, want_chains);
     const uint64_t block_rows = block_chains * 1024;
     uint64_t tc_max = std::max<uint64_t>(min_clocks, tile_bytes / block_rows / 32 * 256);
     tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
     if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
+    if ((rc = tiles.prepare(ctx->stage_bytes))) return rc;
     for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {
         const uint64_t nch = std::min(block_chains, chains - c0);
         const uint64_t row0 = c0 * 1024;
         const uint64_t nrows = std::min<uint64_t>(nch * 1024, ctx->N - row0);
-        for (uint64_t t0 = 0; t0 < T; t0 += tc_max, b ^= 1) {
+        for (uint64_t t0 = 0; t0 < T; t0 += tc_max) {
             const uint64_t tc = std::min(tc_max, T - t0);
             const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
+            const int b = tiles.next();
             if ((rc = acquire_stage(ctx, b))) return rc;
             if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp, c0, nch))) return rc;
-            CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
-            CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
-            uint8_t *dst = out + row0 * pitch_bytes + t0 / 8;
-            if (sp == tc / 8 && pitch_bytes == sp)
-                CK(cudaMemcpyAsync(dst, ctx->d_stage[b], nrows * sp, cudaMemcpyDeviceToHost, ctx->copy));
-            else
-                CK(cudaMemcpy2DAsync(dst, pitch_bytes, ctx->d_stage[b], sp, tc / 8, nrows, cudaMemcpyDeviceToHost,
-                                     ctx->copy));
-            CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
-            ctx->copy_pending[b] = true;
+            if ((rc = tiles.copy_out(b, out + row0 * pitch_bytes + t0 / 8, pitch_bytes, sp, tc / 8, nrows))) return rc;
         }
     }
     return MK2_OK;
@@ -1021,12 +1370,13 @@ static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
     if (pitch_bytes < T / 8) return fail(ctx, MK2_E_ARG, "pitch_bytes smaller than T/8");
     if ((rc = begin_timing(ctx))) return rc;
     const uint64_t chains = (ctx->G + 31) / 32;
-    if (is_device_ptr(out)) {
+    const Mem mem = classify(out);
+    if (mem == Mem::Device) {
         if ((rc = launch_row(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, 0, chains))) return rc;
     } else {
-        int b = 0;
-        if ((rc = rowmajor_to_host(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, b))) return rc;
-        if ((rc = drain_copies(ctx))) return rc;
+        HostTiles tiles(ctx, mem == Mem::Pageable);
+        if ((rc = rowmajor_to_host(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, tiles))) return rc;
+        if ((rc = tiles.finish())) return rc;
     }
     ctx->clocks += T;
     return end_timing(ctx);
@@ -1041,11 +1391,31 @@ static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
 // on three streams, so the upload and the init hide behind the (link-bound) download.
 // The context keeps no resumable state afterwards.
 // ---------------------------------------------------------------------------
+static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride, uint32_t iv_bits,
+                             uint64_t N, uint64_t T, void *out, uint64_t pitch_bytes, uint64_t *checksum);
+
 int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride, uint32_t iv_bits,
                       uint64_t N, uint64_t T, void *out, uint64_t pitch_bytes, uint64_t *checksum)
 {
-    if (!ctx) return MK2_E_ARG;
-    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MK2_E_CUDA, "cudaSetDevice failed");
+    MK2_ENTER(ctx);
+    const int rc = bulk_rowmajor_impl(ctx, keys, ivs, iv_stride, iv_bits, N, T, out, pitch_bytes, checksum);
+    if (rc && rc != MK2_E_ARG) {
+        // a failure part-way through the block pipeline: whatever state is on the device belongs to an arbitrary
+        // block, so the context holds nothing resumable; quiesce the three streams before handing it back
+        ctx->ready = false;
+        ctx->N = ctx->G = 0;
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->copy);
+        if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
+        ctx->copy_pending[0] = ctx->copy_pending[1] = false;
+        cudaGetLastError();
+    }
+    return rc;
+}
+
+static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uint32_t iv_stride, uint32_t iv_bits,
+                             uint64_t N, uint64_t T, void *out, uint64_t pitch_bytes, uint64_t *checksum)
+{
     if (!keys) return fail(ctx, MK2_E_ARG, "keys is NULL");
     if (N == 0) return fail(ctx, MK2_E_ARG, "at least one instance is required");
     if (iv_bits > 80) return fail(ctx, MK2_E_ARG, "IV must be at most 80 bits");
@@ -1054,7 +1424,8 @@ int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uin
     if (!out) return fail(ctx, MK2_E_ARG, "out is NULL");
     if (pitch_bytes < T / 8) return fail(ctx, MK2_E_ARG, "pitch_bytes smaller than T/8");
     int rc;
-    const bool in_dev = is_device_ptr(keys), out_dev = is_device_ptr(out);
+    const Mem out_mem = classify(out);
+    const bool in_dev = is_device_ptr(keys), out_dev = out_mem == Mem::Device;
     if (iv_bits && is_device_ptr(ivs) != in_dev) return fail(ctx, MK2_E_ARG, "keys and ivs must both be host or both be device pointers");
     const uint64_t block_inst = 2ull * 8ull * (uint64_t)ctx->sm_count * 1024ull;  // two chains per worker warp
     if (!ctx->h2d) {
@@ -1083,10 +1454,13 @@ int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uin
     CK(cudaMemsetAsync(ctx->d_sum, 0, sizeof(unsigned long long), ctx->stream));
     CK(cudaEventRecord(ctx->mat_used[0], ctx->stream));  // everything queued before this call is ahead of the uploads
     CK(cudaStreamWaitEvent(ctx->h2d, ctx->mat_used[0], 0));
-    int sb = 0, launches = 0;
+    HostTiles tiles(ctx, out_mem == Mem::Pageable);
+    ctx->row_lsb = false;
+    int launches = 0;
     uint64_t nblk = 0;
     for (uint64_t row0 = 0; row0 < N; row0 += block_inst, ++nblk) {
         const uint64_t n = std::min(block_inst, N - row0);
+        ctx->last_launches = 0;
         const int i = (int)(nblk & 1);
         const uint8_t *dk, *di = nullptr;
         if (in_dev) {
@@ -1112,7 +1486,7 @@ int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uin
         if (out_dev) {
             if ((rc = launch_row(ctx, T, dst, pitch_bytes, 0, (ctx->G + 31) / 32))) return rc;
         } else {
-            if ((rc = rowmajor_to_host(ctx, T, dst, pitch_bytes, sb))) return rc;
+            if ((rc = rowmajor_to_host(ctx, T, dst, pitch_bytes, tiles))) return rc;
         }
         // checksum of the whole call: block sums accumulate in d_sum (block starts are multiples of 64 instances,
         // so the parity term of checksum_kernel is that of the global group index)
@@ -1125,7 +1499,7 @@ int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uin
     CK(cudaMemcpyAsync(&v, ctx->d_sum, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaEventRecord(ctx->ev1, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (!out_dev && (rc = drain_copies(ctx))) return rc;
+    if (!out_dev && (rc = tiles.finish())) return rc;
     CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
     ctx->timing_open = false;
     ctx->last_launches = launches;
@@ -1141,13 +1515,14 @@ int mk2_bulk_rowmajor(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *ivs, uin
 
 int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n)
 {
+    MK2_ENTER(ctx);
     int rc = check_cipher(ctx, 0);
     if (rc) return rc;
     if (n == 0) return MK2_OK;
     if ((rc = begin_timing(ctx))) return rc;
+    Scratch scratch(ctx);
     const uint8_t *din = nullptr;
-    void *owned = nullptr;
-    if ((rc = stage_input(ctx, input_words, input_words ? sizeof(uint32_t) * n * ctx->G : 0, &din, &owned))) return rc;
+    if ((rc = stage_input(ctx, scratch, input_words, input_words ? sizeof(uint32_t) * n * ctx->G : 0, &din))) return rc;
     const uint32_t *w = reinterpret_cast<const uint32_t *>(din);
     if (mixing)
         clock_kernel<true><<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
@@ -1155,13 +1530,13 @@ int mk2_clock(mk2_ctx *ctx, int mixing, const uint32_t *input_words, uint64_t n)
         clock_kernel<false><<<blocks_for(ctx->G, ctx->block), ctx->block, 0, ctx->stream>>>(ctx->d_state, w, n, ctx->G);
     CK(cudaGetLastError());
     ctx->last_launches++;
-    if (owned) CK(cudaFreeAsync(owned, ctx->stream));
     return end_timing(ctx);
 }
 
 int mk2_state_export(mk2_ctx *ctx, uint32_t *rs)
 {
-    int rc = check_ready(ctx);
+    MK2_ENTER(ctx);
+    int rc = check_cipher(ctx, 0);
     if (rc) return rc;
     if (!rs) return fail(ctx, MK2_E_ARG, "rs is NULL");
     const size_t bytes = sizeof(uint32_t) * 2 * NBITS * ctx->G;
@@ -1173,9 +1548,10 @@ int mk2_state_export(mk2_ctx *ctx, uint32_t *rs)
 
 int mk2_state_import(mk2_ctx *ctx, const uint32_t *rs, uint64_t N)
 {
+    MK2_ENTER(ctx);
+    if (!rs) return fail(ctx, MK2_E_ARG, "rs is NULL");
     int rc = init_common(ctx, N);
     if (rc) return rc;
-    if (!rs) return fail(ctx, MK2_E_ARG, "rs is NULL");
     const size_t bytes = sizeof(uint32_t) * 2 * NBITS * ctx->G;
     CK(cudaMemcpyAsync(ctx->d_state, rs, bytes, is_device_ptr(rs) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        ctx->stream));
@@ -1189,6 +1565,7 @@ int mk2_state_import(mk2_ctx *ctx, const uint32_t *rs, uint64_t N)
 
 int mk2_grain_state_export(mk2_ctx *ctx, uint32_t *bs)
 {
+    MK2_ENTER(ctx);
     int rc = check_cipher(ctx, 1);
     if (rc) return rc;
     if (!bs) return fail(ctx, MK2_E_ARG, "bs is NULL");
@@ -1201,6 +1578,7 @@ int mk2_grain_state_export(mk2_ctx *ctx, uint32_t *bs)
 
 int mk2_checksum(mk2_ctx *ctx, uint64_t *sum)
 {
+    MK2_ENTER(ctx);
     int rc = check_ready(ctx);
     if (rc) return rc;
     if (!sum) return fail(ctx, MK2_E_ARG, "sum is NULL");
@@ -1217,8 +1595,8 @@ int mk2_checksum(mk2_ctx *ctx, uint64_t *sum)
 
 int mk2_lop3_peak(mk2_ctx *ctx, double *lane_ops_per_s, float *ms_out)
 {
-    if (!ctx || !lane_ops_per_s) return MK2_E_ARG;
-    CK(cudaSetDevice(ctx->device));
+    if (!lane_ops_per_s) return MK2_E_ARG;
+    MK2_ENTER(ctx);
     uint32_t *sink = nullptr;
     const unsigned nb = 8u * (unsigned)ctx->sm_count;
     CK(cudaMalloc(&sink, sizeof(uint32_t) * nb * BLOCK));

@@ -107,15 +107,37 @@ MK2_HD void static_for_up(F &&f)
     }
 }
 
+// Positions where an all-zero lane does NOT stay all-zero under a zero-input clock: with s = 0 and no
+// feedback, s'[i] = COMP0_i & COMP1_i.  Everything else of CLOCK_KG maps the zero state to itself (R is
+// linear, the control and feedback bits are state bits), so a lane can be held in the zero state by
+// masking these positions only.
+MK2_CX bool zero_leak(int i) { return i >= 1 && i <= 98 && tbit(T_COMP0, i) && tbit(T_COMP1, i); }
+MK2_CX int zero_leak_extra_ops()
+{
+    int n = 0;  // leak positions without a feedback XOR to fold the mask into
+    for (int i = 1; i <= 98; ++i) n += (zero_leak(i) && !tbit(T_FB0, i) && !tbit(T_FB1, i)) ? 1 : 0;
+    return n;
+}
+
 // CLOCK_S of 32 instances, in place (mickey.py:345-358).  fb0 / fb1 are fb_s masked by
 // ~ctrl_s / ctrl_s: the words XORed into FB0-only / FB1-only positions.
-MK2_HD void clock_s(uint32_t (&s)[NBITS], uint32_t fb_s, uint32_t fb0, uint32_t fb1)
+// MASKED: lanes whose `act` bit is clear are lanes still in the all-zero state that must stay there
+// (ragged IV lengths: a lane with a shorter IV starts later); see zero_leak().  The mask rides in the
+// feedback XOR's LOP3 where there is one, so it costs zero_leak_extra_ops() extra LOP3 per clock.
+template <bool MASKED = false>
+MK2_HD void clock_s(uint32_t (&s)[NBITS], uint32_t fb_s, uint32_t fb0, uint32_t fb1, uint32_t act = 0xFFFFFFFFu)
 {
     // s'[i] = s[i-1] ^ ((s[i]^COMP0_i) & (s[i+1]^COMP1_i)) ^ FB
     auto fbmix = [&](auto ic, uint32_t t) -> uint32_t {
         constexpr int i = decltype(ic)::value;
         constexpr bool f0 = tbit(T_FB0, i), f1 = tbit(T_FB1, i);
-        if constexpr (f0 && f1) return t ^ fb_s;
+        if constexpr (MASKED && zero_leak(i)) {
+            constexpr unsigned XOR_AND = ((LA ^ LB) & LC) & 0xFF;  // (a ^ b) & c
+            if constexpr (f0 && f1) return lop3<XOR_AND>(t, fb_s, act);
+            else if constexpr (f0) return lop3<XOR_AND>(t, fb0, act);
+            else if constexpr (f1) return lop3<XOR_AND>(t, fb1, act);
+            else return t & act;
+        } else if constexpr (f0 && f1) return t ^ fb_s;
         else if constexpr (f0) return t ^ fb0;
         else if constexpr (f1) return t ^ fb1;
         else return t;
@@ -284,8 +306,8 @@ MK2_CX int block_lop3_count(int K)
 
 // K x CLOCK_KG.  in_word(k) supplies clock k's input word (INPUT), emit(k, z) receives
 // z = r0 ^ s0 sampled before clock k (EMIT).  Reduced state in, reduced state out.
-template <int K, bool MIXING, bool INPUT, bool EMIT, class In, class Emit>
-MK2_HD void clock_block(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word, Emit &&emit)
+template <int K, bool MIXING, bool INPUT, bool EMIT, bool MASKED, class In, class Emit, class Act>
+MK2_HD void clock_block_impl(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word, Emit &&emit, Act &&act_word)
 {
     static_assert(K >= 1 && K <= MAX_RBLOCK, "block length");
     uint32_t o[K];
@@ -329,7 +351,8 @@ MK2_HD void clock_block(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word
         });
         r[0] &= ctrl_r;
 
-        clock_s(s, fb_s, fb0, fb1);
+        if constexpr (MASKED) clock_s<true>(s, fb_s, fb0, fb1, act_word(kc));
+        else clock_s(s, fb_s, fb0, fb1);
     });
 
     // ---- reduce: r[i] ^= XOR_j Q_j[i] & o[j], the overflow words split in two halves
@@ -344,6 +367,24 @@ MK2_HD void clock_block(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word
         else if constexpr (ma != 0) r[i] ^= ca[ma];
         else if constexpr (mb != 0) r[i] ^= cb[mb];
     });
+}
+
+struct NoAct {
+    template <class KC>
+    MK2_HD uint32_t operator()(KC) const { return 0xFFFFFFFFu; }
+};
+template <int K, bool MIXING, bool INPUT, bool EMIT, class In, class Emit>
+MK2_HD void clock_block(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word, Emit &&emit)
+{
+    clock_block_impl<K, MIXING, INPUT, EMIT, false>(r, s, in_word, emit, NoAct{});
+}
+// K load clocks (mixing, input word in_word(k)) for a group whose lanes start at different clocks:
+// lanes whose bit in act_word(k) is clear are still in the all-zero state, carry a zero input bit and
+// stay in the zero state through clock k.  Costs zero_leak_extra_ops() LOP3 per clock over clock_block.
+template <int K, class In, class Act>
+MK2_HD void clock_block_masked(uint32_t (&r)[NBITS], uint32_t (&s)[NBITS], In &&in_word, Act &&act_word)
+{
+    clock_block_impl<K, true, true, false, true>(r, s, in_word, [](auto, uint32_t) {}, act_word);
 }
 
 // keystream word z_t = r0 ^ s0, sampled before the clock (mickey.py:365-367)

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "mk2_clock.cuh"
+#include "mk2_bits.cuh"
 
 #ifndef MK2_RBLOCK_COL
 #define MK2_RBLOCK_COL 6
@@ -205,13 +206,54 @@ pack_uniform_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict_
 // must end in the all-zero state (from_scalar_states, mickey.py:306-316).
 // mat rows: [0, Lmax+80) input words; [Lmax+80, 2 Lmax+80) activity masks
 // (bit j set once lane j has started); row 2 Lmax+80: final lane mask.
+// fast10 (complete groups, 10-byte IV records, 16-byte aligned arrays): the group's 320 IV bytes and 32
+// lengths come in with 128-bit loads, every lane's bit string is shifted to its start clock with funnel
+// shifts and three 32x32 bit transposes per array turn lanes into clock words (mk2_bits.cuh) -- instead of
+// one byte load and a handful of ALU ops per (lane, clock).
 __global__ void __launch_bounds__(BLOCK)
 pack_ragged_kernel(const uint8_t *__restrict__ keys, const uint8_t *__restrict__ ivs, uint32_t iv_stride,
                    const uint8_t *__restrict__ nbits, int lmax, uint64_t N, uint64_t G,
-                   uint32_t *__restrict__ mat)
+                   uint32_t *__restrict__ mat, bool fast10)
 {
     const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= G) return;
+    if (fast10 && 32 * g + 32 <= N) {
+        uint32_t len[8];
+        {
+            const uint4 *pl = reinterpret_cast<const uint4 *>(nbits + 32 * g);
+            const uint4 a = __ldg(pl), b = __ldg(pl + 1);
+            len[0] = a.x; len[1] = a.y; len[2] = a.z; len[3] = a.w;
+            len[4] = b.x; len[5] = b.y; len[6] = b.z; len[7] = b.w;
+        }
+        uint32_t used = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) used |= (((len[j >> 2] >> (8 * (j & 3))) & 0xFFu) <= 80u ? 1u : 0u) << j;
+        if (lmax > 0) {
+            uint32_t rec[80];
+            const uint4 *p = reinterpret_cast<const uint4 *>(ivs + 320 * g);
+#pragma unroll
+            for (int i = 0; i < 20; ++i) {
+                const uint4 v = __ldg(p + i);
+                rec[4 * i] = v.x; rec[4 * i + 1] = v.y; rec[4 * i + 2] = v.z; rec[4 * i + 3] = v.w;
+            }
+#pragma unroll 1
+            for (int k = 0; 32 * k < lmax; ++k) {
+                uint32_t in[32], act[32];
+                ragged_group_words(rec, len, lmax, k, in, act);
+#pragma unroll
+                for (int b = 0; b < 32; ++b) {
+                    const int c = 32 * k + b;
+                    if (c < lmax) {
+                        mat[(uint64_t)c * G + g] = in[b];
+                        mat[(uint64_t)(lmax + KEY_BITS + c) * G + g] = act[b];
+                    }
+                }
+            }
+        }
+        mat[(uint64_t)(2 * lmax + KEY_BITS) * G + g] = used;
+        pack_records10_to_clocks(keys, KEY_BITS, mat, G, g, lmax);
+        return;
+    }
     uint32_t used = 0;
     int len[32];
 #pragma unroll 1
@@ -287,19 +329,42 @@ init_kernel(const uint32_t *__restrict__ mat, int load_clocks, int lmax, uint64_
     int c = 0;
     uint32_t in_next = load_clocks > 0 ? __ldg(p) : 0u;
     if constexpr (RAGGED) {
+        // IV phase of a group whose lanes start at different clocks: masked blocks (clock_block_masked holds
+        // the lanes that have not started in the all-zero state for 5 extra LOP3 per clock), the next block's
+        // input and activity words in flight while this one runs
         const uint32_t *pa = mat + (uint64_t)(lmax + KEY_BITS) * G + g;
-        uint32_t act_next = lmax > 0 ? __ldg(pa) : 0u;
-#pragma unroll 1
-        for (; c < lmax; ++c) {
-            const uint32_t in = in_next, act = act_next;
-            p += G;
-            pa += G;
-            if (c + 1 < load_clocks) in_next = __ldg(p);
-            if (c + 1 < lmax) act_next = __ldg(pa);
-            clock<true, true>(r, s, in);
+        constexpr int KB = RBLOCK_INIT > 4 ? 4 : RBLOCK_INIT;
+        uint32_t nx[KB], na[KB];
 #pragma unroll
-            for (int i = 0; i < NBITS; ++i) { r[i] &= act; s[i] &= act; }
+        for (int k = 0; k < KB; ++k) {
+            nx[k] = k < lmax ? __ldg(p + (uint64_t)k * G) : 0u;
+            na[k] = k < lmax ? __ldg(pa + (uint64_t)k * G) : 0u;
         }
+#pragma unroll 1
+        for (; c + KB <= lmax; c += KB) {
+            uint32_t cur[KB], act[KB];
+            p += (uint64_t)KB * G;
+            pa += (uint64_t)KB * G;
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+                cur[k] = nx[k];
+                act[k] = na[k];
+                nx[k] = c + KB + k < lmax ? __ldg(p + (uint64_t)k * G) : 0u;
+                na[k] = c + KB + k < lmax ? __ldg(pa + (uint64_t)k * G) : 0u;
+            }
+            clock_block_masked<KB>(
+                r, s, [&](auto kc) { return cur[decltype(kc)::value]; }, [&](auto kc) { return act[decltype(kc)::value]; });
+        }
+#pragma unroll 1
+        for (int k = 0; c < lmax; ++c, ++k) {  // up to KB - 1 single masked clocks; nx / na already hold their words
+            uint32_t w = nx[0], a = na[0];
+#pragma unroll
+            for (int q = 1; q < KB; ++q)
+                if (k == q) { w = nx[q]; a = na[q]; }
+            p += G;
+            clock_block_masked<1>(r, s, [&](auto) { return w; }, [&](auto) { return a; });
+        }
+        in_next = c < load_clocks ? __ldg(p) : 0u;
     }
     if constexpr (RBLOCK_INIT > 1) {
         // blocks of RBLOCK_INIT load clocks (deferred R reduction); the next block's input words are in flight
@@ -827,7 +892,7 @@ __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t 
     }
 }
 
-template <bool ALIGNED16, int TG, int TS>
+template <bool ALIGNED16, int TG, int TS, bool LSB = false>
 __global__ void __launch_bounds__(BLOCK, 1)
 gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
                     unsigned long long *acc_out, uint8_t *__restrict__ out,
@@ -885,7 +950,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     clock<false, false>(r, s, 0u);
                 }
                 hs.fold(a);
-                row_drain<ALIGNED16, TG, TS, false>(col, rows + (t0 >> 3), pitch, ngrp, nrows);
+                row_drain<ALIGNED16, TG, TS, LSB>(col, rows + (t0 >> 3), pitch, ngrp, nrows);
             }
             store_state(state_out, acc_out, G, g, r, s, a);
         }

@@ -158,9 +158,10 @@ __global__ void seed_setup_kernel(const uint8_t *__restrict__ seed /*[32]*/, uin
     }
 }
 
-// One thread per lane: two AES blocks -> 10 key bytes + 10 IV bytes.
+// One thread per lane: two AES blocks -> 10 key bytes + iv_len IV bytes (10 for mickey, 8 for grain:
+// seedgen.py:24-29); the IV rows are iv_len bytes apart.
 __global__ void __launch_bounds__(256)
-seed_derive_kernel(const uint32_t *__restrict__ rk_in, uint32_t tag, uint64_t first_lane, uint64_t n,
+seed_derive_kernel(const uint32_t *__restrict__ rk_in, uint32_t tag, uint64_t first_lane, uint64_t n, int iv_len,
                    uint8_t *__restrict__ keys, uint8_t *__restrict__ ivs)
 {
     __shared__ uint32_t t0r[256 * 32];  // T0, one copy per bank (32 KB)
@@ -187,8 +188,14 @@ seed_derive_kernel(const uint32_t *__restrict__ rk_in, uint32_t tag, uint64_t fi
 #pragma unroll
             for (int w = 0; w < 4; ++w) stream[4 * c + w] = st[w];
         }
-        uint8_t *k = keys + 10 * j, *v = ivs + 10 * j;
-        if (even) {  // 10-byte records at even addresses: five 16-bit stores each instead of ten byte stores
+        uint8_t *k = keys + 10 * j, *v = ivs + (uint64_t)iv_len * j;
+        if (iv_len != 10) {
+#pragma unroll
+            for (int b = 0; b < 10; ++b) k[b] = (uint8_t)(stream[b >> 2] >> (8 * (b & 3)));
+#pragma unroll
+            for (int b = 10; b < 20; ++b)
+                if (b - 10 < iv_len) v[b - 10] = (uint8_t)(stream[b >> 2] >> (8 * (b & 3)));
+        } else if (even) {  // 10-byte records at even addresses: five 16-bit stores each instead of ten byte stores
 #pragma unroll
             for (int u = 0; u < 5; ++u) reinterpret_cast<uint16_t *>(k)[u] = (uint16_t)(stream[u >> 1] >> (16 * (u & 1)));
 #pragma unroll

@@ -165,7 +165,7 @@ __device__ __forceinline__ void close_tile(const uint32_t *smem_slot)
     if ((threadIdx.x >> 5) == 0) dealloc(*smem_slot, blockDim.x > 128 ? 512u : 256u);
 }
 
-template <bool ALIGNED16>
+template <bool ALIGNED16, bool LSB = false>
 __global__ void __launch_bounds__(BLOCK, 1)
 gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
                     unsigned long long *acc_out, uint8_t *__restrict__ out, uint64_t pitch, uint64_t N, uint64_t G,
@@ -219,7 +219,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 }
                 hs.fold(a);
                 wait_st();
-                row_drain<ALIGNED16>(tcol, rows + (t0 >> 3), pitch, ngrp, nrows);
+                row_drain<ALIGNED16, LSB>(tcol, rows + (t0 >> 3), pitch, ngrp, nrows);
             }
             if (real) store_state(state_out, acc_out, G, g, r, s, a);
         }

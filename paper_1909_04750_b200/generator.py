@@ -13,7 +13,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _native
+from . import _native, hostmem
 from ._native import MK2_IV_UNUSED, check
 
 KEY_BYTES = 10
@@ -49,6 +49,8 @@ class MickeyGenerator:
         self._ctx = C.c_void_p()
         check(self._lib.mk2_create(int(device), C.byref(self._ctx)), None, "mk2_create")
         self.device = int(device)
+        self._knobs_touched = False   # hostmem's context pool only keeps contexts in their default configuration
+        self._peak_groups = 0
         if stream is not None:
             self.set_stream(stream)
 
@@ -76,6 +78,7 @@ class MickeyGenerator:
     def set_stream(self, cuda_stream: Optional[int]):
         """Launch on an external CUDA stream handle (e.g. torch.cuda.current_stream().cuda_stream;
         0 is the legacy default stream).  None goes back to the context's own stream."""
+        self._knobs_touched = True
         if cuda_stream is None:
             self._ck(self._lib.mk2_use_own_stream(self._ctx), "mk2_use_own_stream")
         else:
@@ -83,17 +86,21 @@ class MickeyGenerator:
 
     def set_chunk_clocks(self, clocks: int):
         """Tuning knob: clocks per scheduling chunk of the persistent keystream kernels."""
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_chunk_clocks(self._ctx, int(clocks)), "mk2_set_chunk_clocks")
 
     def set_row_staging(self, mode: int):
         """Tuning knob: row-major staging tile in shared memory (1) or tensor memory (2); 0 = automatic."""
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_row_staging(self._ctx, int(mode)), "mk2_set_row_staging")
 
     def set_stage_bytes(self, nbytes: int):
         """Tuning knob: bytes per device staging tile when the output buffer is in host memory."""
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_stage_bytes(self._ctx, int(nbytes)), "mk2_set_stage_bytes")
 
     def set_async(self, flag: bool):
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_async(self._ctx, int(bool(flag))), "mk2_set_async")
 
     def last_plan(self):
@@ -104,6 +111,7 @@ class MickeyGenerator:
 
     def set_block_threads(self, threads: int):
         """Tuning knob: threads per CTA of the clocking kernels (32..256)."""
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_block_threads(self._ctx, int(threads)), "mk2_set_block_threads")
 
     TRACE_DTYPE = np.dtype([("chain", "<u4"), ("k", "<u4"), ("smid", "<u4"), ("warp", "<u4"),
@@ -111,6 +119,7 @@ class MickeyGenerator:
 
     def set_trace(self, capacity: int):
         """Diagnostics: record (chain, chunk, SM, warp, timestamps) per scheduled job."""
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_trace(self._ctx, int(capacity)), "mk2_set_trace")
         self._trace_cap = int(capacity)
 
@@ -122,7 +131,13 @@ class MickeyGenerator:
         return rec[: n.value]
 
     def set_max_ctas(self, ctas: int):
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_max_ctas(self._ctx, int(ctas)), "mk2_set_max_ctas")
+
+    def set_host_threads(self, threads: int):
+        """Host threads that move bounce tiles into PAGEABLE output arrays (0 = automatic)."""
+        self._knobs_touched = True
+        self._ck(self._lib.mk2_set_host_threads(self._ctx, int(threads)), "mk2_set_host_threads")
 
     def synchronize(self):
         self._ck(self._lib.mk2_sync(self._ctx), "mk2_sync")
@@ -132,6 +147,7 @@ class MickeyGenerator:
         self._ck(self._lib.mk2_trim(self._ctx), "mk2_trim")
 
     def set_group_offset(self, group_offset: int):
+        self._knobs_touched = True
         self._ck(self._lib.mk2_set_group_offset(self._ctx, int(group_offset)), "mk2_set_group_offset")
 
     # -- geometry ---------------------------------------------------------
@@ -156,15 +172,19 @@ class MickeyGenerator:
     def init_material(self, keys, ivs=None, iv_bits: int = 0):
         """Uniform IV length: keys u8[N,10], ivs u8[N,>=ceil(iv_bits/8)] (numpy or torch, host or device)."""
         n, iv_stride = _material_shape(keys, ivs, iv_bits)
+        self._note_size(n)
         self._ck(self._lib.mk2_init_from_material(self._ctx, _ptr(keys), _ptr(ivs) if iv_bits else 0, iv_stride,
                                                   int(iv_bits), n), "mk2_init_from_material")
         return self
 
+    def _note_size(self, n: int):
+        self._peak_groups = max(self._peak_groups, (int(n) + 31) // 32)
+
     def init_ragged(self, keys, ivs, iv_nbits):
         """Per-instance IV bit lengths (u8[N], 0..80 or MK2_IV_UNUSED)."""
         n, iv_stride = _material_shape(keys, ivs, 0)
-        if int(np.prod(tuple(iv_nbits.shape))) != n:
-            raise ValueError("iv_nbits must have one entry per instance")
+        iv_nbits = _iv_nbits_u8(iv_nbits, n)
+        self._note_size(n)
         self._ck(self._lib.mk2_init_ragged(self._ctx, _ptr(keys), _ptr(ivs), iv_stride, _ptr(iv_nbits), n),
                  "mk2_init_ragged")
         return self
@@ -174,6 +194,7 @@ class MickeyGenerator:
         if len(key) != KEY_BYTES:
             raise ValueError(f"key must be {KEY_BYTES} bytes")
         kb = (C.c_uint8 * KEY_BYTES).from_buffer_copy(bytes(key))
+        self._note_size(n)
         self._ck(self._lib.mk2_init_counter_iv(self._ctx, C.cast(kb, C.c_void_p), int(first_index), int(n)),
                  "mk2_init_counter_iv")
         return self
@@ -181,17 +202,21 @@ class MickeyGenerator:
     def init_seed(self, seed: bytes, first_lane: int, n: int):
         """Seed-derived key/IV material (seedgen.derive_lane_material) for lanes first_lane..+n-1, then init."""
         sb = _seed_buf(seed)
+        self._note_size(n)
         self._ck(self._lib.mk2_init_from_seed(self._ctx, C.cast(sb, C.c_void_p), int(first_lane), int(n)),
                  "mk2_init_from_seed")
         return self
 
     def derive_material(self, seed: bytes, first_lane: int, n: int, keys=None, ivs=None, algo_tag: int = 3):
-        """keys u8[n,10], ivs u8[n,10] derived on the GPU (numpy by default; torch/device buffers accepted)."""
+        """keys u8[n,10], ivs u8[n,10] (algo_tag 3, mickey) or u8[n,8] (algo_tag 2, grain: seedgen.py:24-29)
+        derived on the GPU (numpy by default; torch/device buffers accepted)."""
         sb = _seed_buf(seed)
+        if algo_tag not in (2, 3):
+            raise ValueError("algo_tag must be 2 (grain) or 3 (mickey)")
         if keys is None:
             keys = np.empty((n, KEY_BYTES), np.uint8)
         if ivs is None:
-            ivs = np.empty((n, 10), np.uint8)
+            ivs = np.empty((n, 10 if algo_tag == 3 else 8), np.uint8)
         self._ck(self._lib.mk2_derive_material(self._ctx, C.cast(sb, C.c_void_p), int(algo_tag), int(first_lane), int(n),
                                                _ptr(keys), _ptr(ivs)), "mk2_derive_material")
         return keys, ivs
@@ -202,24 +227,28 @@ class MickeyGenerator:
         G = self.groups
         stride = G if stride_words is None else int(stride_words)
         if out is None:
-            out = np.empty((nclocks, stride), np.uint32)
+            out = hostmem.empty((nclocks, stride), np.uint32)
         self._ck(self._lib.mk2_generate_colmajor(self._ctx, int(nclocks), _ptr(out), stride), "mk2_generate_colmajor")
         return out
 
-    def generate_rowmajor(self, nclocks: int, out=None, pitch_bytes: Optional[int] = None, byte_offset: int = 0):
-        """uint8 out[N][nclocks/8], MSB-first (the reference's lane-major order)."""
+    def generate_rowmajor(self, nclocks: int, out=None, pitch_bytes: Optional[int] = None, byte_offset: int = 0,
+                          bit_order: str = "msb"):
+        """uint8 out[N][nclocks/8] (the reference's lane-major order); the first bit of every byte in its most
+        significant position, or with bit_order="lsb" in the least significant one (kernels.py:604-612)."""
+        if bit_order not in ("msb", "lsb"):
+            raise ValueError(f"unknown bit order {bit_order!r}")
         if nclocks % 8:
             raise ValueError("bit count must be a multiple of 8")
         N = self.instances
         if out is None:
             pitch = nclocks // 8 if pitch_bytes is None else int(pitch_bytes)
-            out = np.empty((N, pitch), np.uint8)
+            out = hostmem.empty((N, pitch), np.uint8)
         elif pitch_bytes is None:
             pitch = int(out.shape[-1]) * (out.element_size() if _is_torch(out) else out.itemsize)
         else:
             pitch = int(pitch_bytes)
-        self._ck(self._lib.mk2_generate_rowmajor(self._ctx, int(nclocks), _ptr(out) + int(byte_offset), pitch),
-                 "mk2_generate_rowmajor")
+        self._ck(self._lib.mk2_generate_rowmajor_order(self._ctx, int(nclocks), _ptr(out) + int(byte_offset), pitch,
+                                                       int(bit_order == "lsb")), "mk2_generate_rowmajor_order")
         return out
 
     def bulk_rowmajor(self, keys, ivs, iv_bits: int, nclocks: int, out=None, pitch_bytes: Optional[int] = None):
@@ -229,9 +258,10 @@ class MickeyGenerator:
         if nclocks % 8:
             raise ValueError("bit count must be a multiple of 8")
         n, iv_stride = _material_shape(keys, ivs, iv_bits)
+        self._note_size(min(n, 1 << 22))
         if out is None:
             pitch = nclocks // 8 if pitch_bytes is None else int(pitch_bytes)
-            out = np.empty((n, pitch), np.uint8)
+            out = hostmem.empty((n, pitch), np.uint8)
         elif pitch_bytes is None:
             pitch = int(out.shape[-1]) * (out.element_size() if _is_torch(out) else out.itemsize)
         else:
@@ -253,6 +283,7 @@ class MickeyGenerator:
         return rs
 
     def import_state(self, rs, n: int):
+        self._note_size(n)
         rs = np.ascontiguousarray(rs, np.uint32) if isinstance(rs, np.ndarray) else rs
         self._ck(self._lib.mk2_state_import(self._ctx, _ptr(rs), int(n)), "mk2_state_import")
         return self
@@ -276,6 +307,28 @@ class MickeyGenerator:
         v, ms = C.c_double(), C.c_float()
         self._ck(self._lib.mk2_lop3_peak(self._ctx, C.byref(v), C.byref(ms)), "mk2_lop3_peak")
         return v.value, ms.value
+
+
+def _iv_nbits_u8(iv_nbits, n: int):
+    """Per-instance IV bit lengths as the C ABI reads them: n contiguous uint8 values (0..80 or MK2_IV_UNUSED).
+    Lists and integer numpy arrays of any width are range-checked and converted (a default int64 array read as
+    raw bytes would silently load wrong lengths); torch tensors must already be uint8."""
+    if _is_torch(iv_nbits):
+        if _dtype_name(iv_nbits) != "uint8" or iv_nbits.numel() != n:
+            raise ValueError("iv_nbits must be a uint8 tensor with one entry per instance")
+        return iv_nbits.contiguous()
+    a = np.asarray(iv_nbits)
+    if a.size != n:
+        raise ValueError("iv_nbits must have one entry per instance")
+    if a.dtype == np.uint8:
+        return np.ascontiguousarray(a).reshape(-1)
+    if not np.issubdtype(a.dtype, np.integer):
+        raise ValueError("iv_nbits must hold integers")
+    a = a.reshape(-1)
+    bad = np.flatnonzero(((a < 0) | (a > IV_MAX_BITS)) & (a != MK2_IV_UNUSED))
+    if bad.size:
+        raise ValueError(f"lane {int(bad[0])}: IV must be at most {IV_MAX_BITS} bits")
+    return np.ascontiguousarray(a.astype(np.uint8))
 
 
 def _seed_buf(seed: bytes):

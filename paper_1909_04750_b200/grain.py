@@ -14,6 +14,7 @@ from typing import Sequence
 
 import numpy as np
 
+from . import hostmem
 from .generator import MickeyGenerator, _ptr
 from .mickey import LANE_WIDTHS, LaneState  # noqa: F401  (LaneState re-exported for extract_lane users)
 
@@ -73,6 +74,7 @@ class GrainGenerator(MickeyGenerator):
             raise ValueError("keys must be [N, 10] and ivs [N, 8]")
         if kshape[0] < 1:
             raise ValueError("at least one lane is required")
+        self._note_size(kshape[0])
         self._ck(self._lib.mk2_grain_init_from_material(self._ctx, _ptr(keys), _ptr(ivs), kshape[0]),
                  "mk2_grain_init_from_material")
         return self
@@ -81,7 +83,7 @@ class GrainGenerator(MickeyGenerator):
         G = self.groups
         stride = G if stride_words is None else int(stride_words)
         if out is None:
-            out = np.empty((nclocks, stride), np.uint32)
+            out = hostmem.empty((nclocks, stride), np.uint32)
         self._ck(self._lib.mk2_grain_generate_colmajor(self._ctx, int(nclocks), _ptr(out), stride),
                  "mk2_grain_generate_colmajor")
         return out
@@ -93,7 +95,7 @@ class GrainGenerator(MickeyGenerator):
             raise ValueError("bit count must be a multiple of 8")
         if out is None:
             pitch = nclocks // 8 if pitch_bytes is None else int(pitch_bytes)
-            out = np.empty((self.instances, pitch), np.uint8)
+            out = hostmem.empty((self.instances, pitch), np.uint8)
         elif pitch_bytes is None:
             pitch = int(out.shape[-1])
         else:
@@ -136,6 +138,14 @@ class GrainSliced:
         self.width = width
         self.mask = (1 << width) - 1
 
+    def __del__(self):
+        gen, self._gen = getattr(self, "_gen", None), None
+        if gen is not None:
+            try:
+                hostmem.release_context(gen)   # back to this thread's idle contexts (hostmem.py)
+            except Exception:  # interpreter shutdown
+                pass
+
     @classmethod
     def from_key_ivs(cls, materials: Sequence[GrainKeyIv], width: int = 64, device: int = 0) -> "GrainSliced":
         if width not in LANE_WIDTHS:
@@ -143,8 +153,12 @@ class GrainSliced:
         keys, ivs = pack_materials(materials, width)
         # lanes beyond len(materials) are the reference's unused lanes: the generator is sized to the
         # lane count, and the kernel leaves the rest of the group without the LFSR's top ones
-        gen = GrainGenerator(device)
-        gen.init_material(keys, ivs)
+        gen = hostmem.acquire_context(GrainGenerator, device)
+        try:
+            gen.init_material(keys, ivs)
+        except BaseException:
+            gen.close()
+            raise
         return cls(gen, width)
 
     def _words(self):

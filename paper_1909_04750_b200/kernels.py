@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import mickey
+from . import hostmem, mickey
 from .generator import MickeyGenerator
 
 _U64 = np.uint64
@@ -24,32 +24,41 @@ def mickey_sliced_words(materials, nclocks: int, width: int = 64, device: int = 
     Every call restarts from init, like the reference's compiled loop; odd
     `nclocks` is fine; at width 32 the high 32 bits are zero.
     """
-    eng = mickey.MickeySliced.from_key_ivs(materials, width, device=device)
-    if nclocks == 0:
-        return np.zeros(0, np.uint64)
-    out = eng._gen.generate_colmajor(int(nclocks))
-    return mickey._as_u64(out)
+    if width not in mickey.LANE_WIDTHS:
+        raise ValueError(f"lane width must be one of {mickey.LANE_WIDTHS}")
+    keys, ivs, nbits, uniform = mickey.pack_materials(materials, width)
+    with hostmem.borrow_context(MickeyGenerator, device) as gen:   # an idle context of this thread when there is one
+        if uniform:
+            gen.init_material(keys, ivs, int(nbits[0]))
+        else:
+            gen.init_ragged(keys, ivs, nbits)
+        if nclocks == 0:
+            return np.zeros(0, np.uint64)
+        return mickey._as_u64(gen.generate_colmajor(int(nclocks)))
 
 
 def bulk_colmajor(keys, ivs, iv_bits, nclocks: int, device: int = 0, out=None):
     """N instances (u8[N,10] keys, u8[N,*] ivs) -> uint32 out[nclocks][ceil(N/32)].
 
     iv_bits: one int (uniform) or a u8[N] array (ragged)."""
-    with MickeyGenerator(device) as gen:
+    with hostmem.borrow_context(MickeyGenerator, device) as gen:
         _init(gen, keys, ivs, iv_bits)
         return gen.generate_colmajor(nclocks, out)
 
 
-def bulk_rowmajor(keys, ivs, iv_bits, nclocks: int, device: int = 0, out=None):
-    """N instances -> uint8 out[N][nclocks/8], MSB-first rows (lane-major order).
+def bulk_rowmajor(keys, ivs, iv_bits, nclocks: int, device: int = 0, out=None, bit_order: str = "msb"):
+    """N instances -> uint8 out[N][nclocks/8], lane-major rows; bit_order as in words_lane_major_bytes
+    (kernels.py:615-621: first bit of a byte in its most ("msb", default) or least ("lsb") significant position).
 
-    Uniform IV length: one mk2_bulk_rowmajor call (upload, init + keystream and download of consecutive
-    instance blocks overlap); ragged IV lengths: init, then generate."""
-    with MickeyGenerator(device) as gen:
-        if np.isscalar(iv_bits) and nclocks > 0:
+    Uniform IV length, MSB-first: one mk2_bulk_rowmajor call (upload, init + keystream and download of consecutive
+    instance blocks overlap); otherwise init, then generate."""
+    if bit_order not in ("msb", "lsb"):
+        raise ValueError(f"unknown bit order {bit_order!r}")
+    with hostmem.borrow_context(MickeyGenerator, device) as gen:
+        if np.isscalar(iv_bits) and nclocks > 0 and bit_order == "msb":
             return gen.bulk_rowmajor(keys, ivs, int(iv_bits), nclocks, out)[0]
         _init(gen, keys, ivs, iv_bits)
-        return gen.generate_rowmajor(nclocks, out)
+        return gen.generate_rowmajor(nclocks, out, bit_order=bit_order)
 
 
 def _init(gen, keys, ivs, iv_bits):

@@ -14,6 +14,7 @@ from typing import Sequence
 
 import numpy as np
 
+from . import hostmem
 from ._native import MK2_IV_UNUSED
 from .generator import MickeyGenerator
 
@@ -147,8 +148,18 @@ class MickeySliced:
             raise ValueError("sliced state needs 100 R words and 100 S words")
         self.width = width
         self.mask = (1 << width) - 1
-        self._gen = MickeyGenerator(device)
+        self._gen = hostmem.acquire_context(MickeyGenerator, device)
         self._gen.import_state(self._words_to_rs(rregs, sregs), width)
+
+    def __del__(self):
+        # the context goes back to this thread's pool of idle contexts (hostmem.py) instead of being destroyed:
+        # the reference's callers build one engine per 64-lane batch (cli.py:219-231)
+        gen, self._gen = getattr(self, "_gen", None), None
+        if gen is not None:
+            try:
+                hostmem.release_context(gen)
+            except Exception:  # interpreter shutdown
+                pass
 
     @classmethod
     def _adopt(cls, gen: MickeyGenerator, width: int) -> "MickeySliced":
@@ -173,11 +184,15 @@ class MickeySliced:
         if width not in LANE_WIDTHS:
             raise ValueError(f"lane width must be one of {LANE_WIDTHS}")
         keys, ivs, nbits, uniform = pack_materials(materials, width)
-        gen = MickeyGenerator(device)
-        if uniform:
-            gen.init_material(keys, ivs, int(nbits[0]))
-        else:
-            gen.init_ragged(keys, ivs, nbits)
+        gen = hostmem.acquire_context(MickeyGenerator, device)
+        try:
+            if uniform:
+                gen.init_material(keys, ivs, int(nbits[0]))
+            else:
+                gen.init_ragged(keys, ivs, nbits)
+        except BaseException:
+            gen.close()
+            raise
         return cls._adopt(gen, width)
 
     # -- state views ------------------------------------------------------

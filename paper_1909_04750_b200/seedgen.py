@@ -13,6 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import hostmem
 from .generator import MickeyGenerator
 from .mickey import MickeyKeyIv
 
@@ -52,7 +53,7 @@ def derive_arrays(master: MasterSeed, first_lane: int = 0, n: int | None = None,
     n = master.lanes - first_lane if n is None else n
     if first_lane < 0 or n < 1 or first_lane + n > master.lanes:
         raise IndexError(f"lanes [{first_lane}, {first_lane + n}) out of range [0, {master.lanes})")
-    with MickeyGenerator(device) as gen:
+    with hostmem.borrow_context(MickeyGenerator, device) as gen:
         return gen.derive_material(master.seed, first_lane, n)
 
 

@@ -54,10 +54,10 @@ def parse_vector_file(text: str, algo: str = "mickey", bit_order: str = "msb"):
         if not line:
             continue
         fields = dict(part.split("=", 1) for part in line.split() if "=" in part)
-        if not {"key", "iv", "ks"} <= set(fields):
+        if not {"key", "ks"} <= set(fields):
             raise ValueError(f"line {lineno}: expected key=<hex> iv=<hex> ks=<hex>")
-        try:
-            records.append(VectorRecord(algo, bytes.fromhex(fields["key"]), bytes.fromhex(fields["iv"]),
+        try:   # a missing iv= means the empty IV (vectors.py:120)
+            records.append(VectorRecord(algo, bytes.fromhex(fields["key"]), bytes.fromhex(fields.get("iv", "")),
                                         bytes.fromhex(fields["ks"]), bit_order))
         except ValueError as exc:
             raise ValueError(f"line {lineno}: {exc}") from exc

@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "../paper_1909_04750_b200/csrc/mk2_clock.cuh"
+#include "../paper_1909_04750_b200/csrc/mk2_bits.cuh"
 
 using namespace mk2;
 
@@ -59,6 +60,30 @@ int hc_block(int K, uint32_t *r, uint32_t *s, int mixing, int has_in, const uint
     default: return -1;
     }
 }
+// one clock_block_masked<K> (load clocks of a ragged group: lanes with a clear act bit stay in the zero state)
+int hc_block_masked(int K, uint32_t *r, uint32_t *s, const uint32_t *in, const uint32_t *act)
+{
+    auto &R = *reinterpret_cast<uint32_t(*)[NBITS]>(r);
+    auto &S = *reinterpret_cast<uint32_t(*)[NBITS]>(s);
+    auto inw = [&](auto kc) { return in[decltype(kc)::value]; };
+    auto actw = [&](auto kc) { return act[decltype(kc)::value]; };
+    switch (K) {
+    case 1: clock_block_masked<1>(R, S, inw, actw); return 0;
+    case 2: clock_block_masked<2>(R, S, inw, actw); return 0;
+    case 3: clock_block_masked<3>(R, S, inw, actw); return 0;
+    case 4: clock_block_masked<4>(R, S, inw, actw); return 0;
+    default: return -1;
+    }
+}
+void hc_transpose32(uint32_t *a) { transpose32(*reinterpret_cast<uint32_t(*)[32]>(a)); }
+// fast path of pack_ragged_kernel for one group: 96 input words + 96 activity words (clock-major)
+void hc_ragged_group(const uint32_t *rec, const uint32_t *len, int lmax, uint32_t *in96, uint32_t *act96)
+{
+    for (int k = 0; k < 3; ++k)
+        ragged_group_words(*reinterpret_cast<const uint32_t(*)[80]>(rec), *reinterpret_cast<const uint32_t(*)[8]>(len), lmax, k,
+                           *reinterpret_cast<uint32_t(*)[32]>(in96 + 32 * k), *reinterpret_cast<uint32_t(*)[32]>(act96 + 32 * k));
+}
+int hc_zero_leak_extra_ops() { return zero_leak_extra_ops(); }
 int hc_block_lop3_count(int K) { return K >= 1 && K <= MAX_RBLOCK ? block_lop3_count(K) : -1; }
 int hc_q_bit(int j, int i) { return qbit(j, i) ? 1 : 0; }
 }

@@ -27,6 +27,9 @@ def hc(tmp_path_factory):
     lib = C.CDLL(str(so))
     lib.hc_plain.argtypes = [u32p, u32p, C.c_int, C.c_int, u32p, C.c_int, u32p]
     lib.hc_block.argtypes = [C.c_int, u32p, u32p, C.c_int, C.c_int, u32p, u32p]
+    lib.hc_block_masked.argtypes = [C.c_int, u32p, u32p, u32p, u32p]
+    lib.hc_transpose32.argtypes = [u32p]
+    lib.hc_ragged_group.argtypes = [u32p, u32p, C.c_int, u32p, u32p]
     return lib
 
 
@@ -88,3 +91,62 @@ def test_block_costs_fewer_lop3_than_plain_clocks(hc):
     for K in range(2, 7):
         assert counts[K] / K < counts[K - 1] / (K - 1)
     assert counts[4] == 1213 and counts[5] == 1503 and counts[6] == 1794
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4])
+def test_masked_block_holds_late_lanes_in_the_zero_state(hc, K):
+    """clock_block_masked<K> (ragged IV lengths: a lane with a shorter IV joins later) against the plain
+    semantics -- clock every lane, then force the lanes that have not started back to zero -- and, lane by lane,
+    against the oracle's engine started at the lane's own first clock (mickey.py:287-289: per-lane init)."""
+    rng = random.Random(77 + K)
+    nclocks = 3 * K
+    for trial in range(6):
+        start = [rng.randrange(0, nclocks + 1) for _ in range(32)]        # lane j's first active clock
+        act = np.array([sum((c >= start[j]) << j for j in range(32)) for c in range(nclocks)], np.uint32)
+        words = np.array([rng.getrandbits(32) for _ in range(nclocks)], np.uint32) & act   # idle lanes carry zero input
+        r = np.zeros(100, np.uint32)
+        s = np.zeros(100, np.uint32)
+        rp, sp = r.copy(), s.copy()
+        z = np.zeros(1, np.uint32)
+        for c in range(nclocks):                                          # reference semantics, one clock at a time
+            hc.hc_plain(_p(rp), _p(sp), 1, 1, _p(words[c:c + 1].copy()), 1, _p(z))
+            rp &= act[c]
+            sp &= act[c]
+        for b in range(nclocks // K):
+            assert hc.hc_block_masked(K, _p(r), _p(s), _p(words[b * K:(b + 1) * K].copy()), _p(act[b * K:(b + 1) * K].copy())) == 0
+        assert np.array_equal(r, rp) and np.array_equal(s, sp)
+        for j in (0, 7, 31):                                              # per-lane: the oracle started at clock start[j]
+            eng = orc.Sliced()
+            for c in range(start[j], nclocks):
+                eng.clock_kg(True, (int(words[c]) >> j) & 1)
+            assert [(int(x) >> j) & 1 for x in r] == [int(x) & 1 for x in eng._st[:100]]
+            assert [(int(x) >> j) & 1 for x in s] == [int(x) & 1 for x in eng._st[100:]]
+    assert hc.hc_zero_leak_extra_ops() == 5
+
+
+def test_transpose32_and_ragged_group_packing(hc):
+    """The bit-matrix helpers of pack_ragged_kernel's fast path (csrc/mk2_bits.cuh) against plain Python: lane j
+    with L_j IV bits idles for lmax - L_j clocks and then feeds its IV bits MSB-first (bitops.py:33-36)."""
+    rng = random.Random(5)
+    a = np.array([rng.getrandbits(32) for _ in range(32)], np.uint32)
+    t = a.copy()
+    hc.hc_transpose32(_p(t))
+    assert all(((int(t[b]) >> j) & 1) == ((int(a[j]) >> b) & 1) for b in range(32) for j in range(32))
+    for trial in range(20):
+        ivs = np.array([[rng.getrandbits(8) for _ in range(10)] for _ in range(32)], np.uint8)
+        lens = [rng.choice([0, 1, 7, 8, 31, 32, 33, 63, 64, 65, 79, 80, 0xFF, rng.randrange(81)]) for _ in range(32)]
+        real = [l for l in lens if l <= 80]
+        lmax = max(real) if real and trial % 5 else 80
+        inw = np.zeros(96, np.uint32)
+        act = np.zeros(96, np.uint32)
+        hc.hc_ragged_group(_p(ivs.reshape(-1).view("<u4").copy()), _p(np.array(lens, np.uint8).view("<u4").copy()), lmax,
+                           _p(inw), _p(act))
+        for c in range(96):
+            want_in = want_act = 0
+            for j, L in enumerate(lens):
+                if L > 80 or c >= lmax or c < lmax - L:
+                    continue
+                want_act |= 1 << j
+                cc = c - (lmax - L)
+                want_in |= ((int(ivs[j, cc >> 3]) >> (7 - (cc & 7))) & 1) << j
+            assert int(inw[c]) == want_in and int(act[c]) == want_act, (trial, c)

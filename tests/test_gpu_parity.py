@@ -1125,3 +1125,193 @@ def test_acceptance_thousand_random_instances(pkg, oracle):
     for n in (0, 499, 999):                      # and the bit-serial engine agrees on single instances
         st = oracle.Scalar.from_key_iv(keys[n].tobytes(), ivs[n, : nbits[n] // 8].tobytes())
         assert st.keystream_bytes(T // 8) == got[n].tobytes()
+
+
+# ---------------------------------------------------------------- round 2: host buffers, ragged at scale, LSB rows, faults
+
+def test_pageable_host_outputs_go_through_bounce_tiles(pkg, oracle):
+    """Caller-owned PAGEABLE numpy arrays (what kernels.py:194-200 returns) large enough for the pinned bounce
+    pipeline: several staging tiles per call, column-major (contiguous and strided), row-major (pitched) and the
+    one-shot bulk call -- all bit-exact against the oracle; the pool-backed default arrays agree."""
+    N, T = 16384 + 96, 4096
+    keys, ivs = random_arrays(77, N)
+    want_c = oracle.bulk_colmajor(keys, ivs, 80, T)
+    want_r = oracle.bulk_rowmajor(keys, ivs, 80, T)
+    G = (N + 31) // 32
+    with pkg.MickeyGenerator(0) as gen:
+        gen.set_stage_bytes(1 << 20)                                   # 8 MiB of output = 8 column tiles
+        gen.set_host_threads(3)
+        out = np.empty((T, G), np.uint32)                              # pageable, first touched by the copy workers
+        gen.init_material(keys, ivs, 80).generate_colmajor(T, out)
+        assert np.array_equal(out, want_c)
+        wide = np.zeros((T, G + 5), np.uint32)
+        gen.init_material(keys, ivs, 80).generate_colmajor(T, wide, stride_words=G + 5)
+        assert np.array_equal(wide[:, :G], want_c) and not wide[:, G:].any()
+        rows = np.zeros((N, T // 8 + 24), np.uint8)
+        gen.init_material(keys, ivs, 80).generate_rowmajor(T, rows)
+        assert np.array_equal(rows[:, : T // 8], want_r) and not rows[:, T // 8:].any()
+        rows2 = np.empty((N, T // 8), np.uint8)
+        _, csum = gen.bulk_rowmajor(keys, ivs, 80, T, rows2)
+        assert np.array_equal(rows2, want_r) and csum == oracle.checksum_colmajor(want_c)
+        gen.set_host_threads(1)                                        # the calling thread alone
+        out[:] = 0
+        gen.init_material(keys, ivs, 80).generate_colmajor(T, out)
+        assert np.array_equal(out, want_c)
+        # default result arrays: page-locked blocks from the pool (direct D2H), owned by the caller
+        a = gen.init_material(keys, ivs, 80).generate_colmajor(T)
+        b = gen.init_material(keys, ivs, 80).generate_rowmajor(T)
+        assert np.array_equal(a, want_c) and np.array_equal(b, want_r)
+    from paper_1909_04750_b200 import hostmem
+    allocs = hostmem.pool.allocs
+    del a, b                                                           # blocks go back to the cache ...
+    with pkg.MickeyGenerator(0) as gen:
+        c = gen.init_material(keys, ivs, 80).generate_colmajor(T)      # ... and are reused without a new allocation
+        assert np.array_equal(c, want_c) and hostmem.pool.allocs == allocs
+
+
+def test_rowmajor_lsb_bit_order(pkg, oracle):
+    """bit_order="lsb" of words_to_lane_bytes / words_lane_major_bytes (kernels.py:604-621) straight from the GPU:
+    the tensor-memory kernel, the shared-memory kernel, ragged tails and the host mirror's helpers agree."""
+    N, T = 2048 + 40, 1024 + 136
+    keys, ivs = random_arrays(31, N)
+    msb = oracle.bulk_rowmajor(keys, ivs, 80, T)
+    want = np.packbits(np.unpackbits(msb, axis=1), axis=1, bitorder="little")
+    for staging in (0, 1):
+        with pkg.MickeyGenerator(0) as gen:
+            gen.set_row_staging(staging)
+            got = gen.init_material(keys, ivs, 80).generate_rowmajor(T, bit_order="lsb")
+            assert np.array_equal(got, want), staging
+            assert np.array_equal(gen.init_material(keys, ivs, 80).generate_rowmajor(T), msb)
+    assert np.array_equal(pkg.bulk_rowmajor(keys, ivs, 80, T, bit_order="lsb"), want)
+    words = pkg.mickey_sliced_words([pkg.MickeyKeyIv(keys[j].tobytes(), ivs[j].tobytes()) for j in range(64)], T)
+    assert pkg.words_lane_major_bytes(words, 64, "lsb") == want[:64].tobytes()
+    with pytest.raises(ValueError):
+        pkg.bulk_rowmajor(keys, ivs, 80, T, bit_order="big")
+
+
+def test_ragged_iv_lengths_at_scale(pkg, oracle, torch_cuda):
+    """The reference's acceptance workload shape (random IV length of 0..10 bytes per instance,
+    tests/test_acceptance.py:103-135) at 2^17 instances, plus bit-granular lengths and unused lanes: the
+    vectorised packing + masked-block init against the oracle's per-lane scalar init, every instance
+    (whole-job checksum) and sampled rows; device-resident inputs take the same path."""
+    torch = torch_cuda
+    N, T = 1 << 17, 256
+    rng = np.random.default_rng(2024)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    for name, nbits in (("bytes", (8 * rng.integers(0, 11, N)).astype(np.uint8)),
+                        ("bits", rng.integers(0, 81, N).astype(np.uint8)),
+                        ("short", rng.integers(0, 24, N).astype(np.uint8))):
+        want = oracle.checksum_material(keys, ivs, nbits, T)
+        with pkg.MickeyGenerator(0) as gen:
+            gen.init_ragged(keys, ivs, nbits)
+            col = gen.generate_colmajor(T)
+            assert gen.checksum() == want, name
+            assert int(col.view("<u8").sum(dtype=np.uint64)) == want, name
+            idx = np.unique(np.concatenate([[0, 31, 32, N - 1], rng.integers(0, N, 200)]))
+            gen.init_ragged(torch.from_numpy(keys).cuda(), torch.from_numpy(ivs).cuda(), torch.from_numpy(nbits).cuda())
+            rows = gen.generate_rowmajor(T)
+            assert gen.checksum() == want, name
+            for n in idx:
+                lane = oracle.bulk_rowmajor(keys[n:n + 1], ivs[n:n + 1], nbits[n:n + 1], T)[0]
+                assert np.array_equal(rows[n], lane), (name, n)
+    # int64 lengths (numpy's default) are converted, not read as raw bytes; out-of-range values are rejected
+    with pkg.MickeyGenerator(0) as gen:
+        a = gen.init_ragged(keys[:96], ivs[:96], nbits[:96].astype(np.int64)).generate_colmajor(64)
+        b = gen.init_ragged(keys[:96], ivs[:96], nbits[:96].tolist()).generate_colmajor(64)
+        c = gen.init_ragged(keys[:96], ivs[:96], nbits[:96]).generate_colmajor(64)
+        assert np.array_equal(a, c) and np.array_equal(b, c)
+        with pytest.raises(ValueError, match="lane 7"):
+            bad = nbits[:96].astype(np.int64)
+            bad[7] = 300
+            gen.init_ragged(keys[:96], ivs[:96], bad)
+
+
+def test_failures_leave_the_context_usable(pkg, oracle, torch_cuda):
+    """Fault injection through the C ABI: an init that cannot get its state arrays (NOMEM), a host-output call
+    that cannot get its staging tiles, bad arguments in the middle of a session.  Afterwards the same context
+    must report 'no material' (not launch on freed buffers) and then work normally."""
+    torch = torch_cuda
+    keys, ivs = random_arrays(5, 4096)
+    want = oracle.bulk_colmajor(keys, ivs, 80, 128)
+    gen = pkg.MickeyGenerator(0)
+    gen.init_material(keys, ivs, 80)
+    with pytest.raises(pkg.Mk2Error, match="code -5"):                 # 2^35 instances = 860 GB of state
+        gen.init_counter(bytes(10), 0, 1 << 35)
+    with pytest.raises(pkg.Mk2Error, match="no key/IV material"):      # the old state is gone, and known to be gone
+        gen.generate_colmajor(8)
+    with pytest.raises(pkg.Mk2Error, match="no key/IV material"):
+        gen.checksum()
+    assert np.array_equal(gen.init_material(keys, ivs, 80).generate_colmajor(128), want)
+    # staging tiles that do not fit: fill the device, ask for a host output that needs 2 x 1 GiB of staging
+    big_n = 1 << 21
+    gen.init_counter(bytes(10), 0, big_n)
+    gen.set_stage_bytes(1 << 30)
+    free = torch.cuda.mem_get_info()[0]
+    hog = torch.empty(max(0, free - (768 << 20)), dtype=torch.uint8, device="cuda")
+    host = np.empty((8192, big_n // 32), np.uint32)
+    with pytest.raises(pkg.Mk2Error, match="code -5"):
+        gen.generate_colmajor(8192, host)
+    del hog
+    torch.cuda.empty_cache()
+    gen.set_stage_bytes(0)
+    ref = pkg.MickeyGenerator(0)
+    a = gen.init_counter(bytes(10), 0, 4096).generate_colmajor(256)
+    b = ref.init_counter(bytes(10), 0, 4096).generate_colmajor(256)
+    assert np.array_equal(a, b)
+    # bulk call failing on its arguments does not clobber the live state
+    gen.init_material(keys, ivs, 80)
+    with pytest.raises(ValueError):
+        gen.bulk_rowmajor(keys, ivs, 80, 12)                            # not a multiple of 8 (Python-side check)
+    with pytest.raises(ValueError):
+        gen._ck(gen._lib.mk2_bulk_rowmajor(gen._ctx, keys.ctypes.data, ivs.ctypes.data, 10, 80, 4096, 64, 0, 8, None),
+                "mk2_bulk_rowmajor")                                    # NULL out
+    assert np.array_equal(gen.generate_colmajor(128), want)
+    # derivation tags (seedgen.py:24-31): aes-ctr and unknown tags are rejected before anything is allocated
+    for tag in (0, 1, 4):
+        with pytest.raises(ValueError):
+            gen.derive_material(bytes(range(32)), 0, 8, algo_tag=tag)
+    kg, ig = gen.derive_material(bytes(range(32)), 0, 8, algo_tag=2)
+    assert kg.shape == (8, 10) and ig.shape == (8, 8)
+    wk, wi = oracle.derive_material(bytes(range(32)), 0, 8, tag=2)
+    assert np.array_equal(kg, wk) and np.array_equal(ig, wi[:, :8])
+    gen.close()
+    ref.close()
+
+
+def test_entry_points_restore_the_callers_device(pkg, torch_cuda):
+    """Every C-ABI entry point runs under a device guard: the caller's current device is unchanged."""
+    torch = torch_cuda
+    before = torch.cuda.current_device()
+    with pkg.MickeyGenerator(0) as gen:
+        gen.init_counter(bytes(10), 0, 64).generate_colmajor(8)
+        gen.checksum()
+    assert torch.cuda.current_device() == before
+    x = torch.ones(4, device="cuda")
+    assert x.device.index == before and float(x.sum()) == 4.0
+
+
+def test_reference_shaped_calls_reuse_idle_contexts(pkg, golden):
+    """mickey_sliced_words / MickeySliced.from_key_ivs in the reference's 64-lane batching pattern
+    (cli.py:219-231) take an idle context of the thread instead of creating and destroying one per call."""
+    from paper_1909_04750_b200 import hostmem
+    from paper_1909_04750_b200.generator import MickeyGenerator
+    hostmem.drop_idle_contexts()
+    rec = golden["kats"][0]
+    mats = [pkg.MickeyKeyIv(bytes.fromhex(rec["key"]), bytes.fromhex(rec["iv"]))] * 64
+    w1 = pkg.mickey_sliced_words(mats, 128)
+    idle = hostmem._idle((MickeyGenerator, 0))
+    assert len(idle) == 1
+    ctx = idle[0]._ctx.value
+    for _ in range(3):
+        assert np.array_equal(pkg.mickey_sliced_words(mats, 128), w1)
+    assert len(idle) == 1 and idle[0]._ctx.value == ctx              # the same context served every call
+    eng = pkg.MickeySliced.from_key_ivs(mats, 64)
+    assert len(idle) == 0 and eng._gen._ctx.value == ctx
+    eng2 = pkg.MickeySliced.from_key_ivs(mats, 64)                     # a second live engine gets its own
+    assert eng2._gen._ctx.value != ctx
+    assert eng.keystream_words(16) == eng2.keystream_words(16) == [int(w) for w in w1[:16]]
+    del eng, eng2
+    assert len(idle) == 2
+    assert pkg.words_to_lane_bytes(w1, 5)[:16].hex() == rec["ks"]
+    hostmem.drop_idle_contexts()

@@ -22,7 +22,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for name in sorted(declared):
         assert hasattr(L, name), f"libmk2.so does not export {name}"
     assert declared == set(_native.SYMBOLS), "ctypes table out of sync with include/mk2.h"
-    assert _native.lib().mk2_abi_version() == 1
+    assert _native.lib().mk2_abi_version() == _native.ABI_VERSION == 2
     assert _native.lib().mk2_lop3_per_clock() == 327
 
 

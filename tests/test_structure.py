@@ -46,8 +46,8 @@ def _innermost_clock_loops(ins, lo_lop3, hi_lop3):
     return loops
 
 
-@pytest.mark.parametrize("kernel", ["mk219gen_colmajor_kernel", "mk219gen_rowmajor_kernelILb1ELi32ELi224E",
-                                    "mk24tmem19gen_rowmajor_kernelILb1E"])
+@pytest.mark.parametrize("kernel", ["mk219gen_colmajor_kernel", "mk219gen_rowmajor_kernelILb1ELi32ELi224ELb0E",
+                                    "mk24tmem19gen_rowmajor_kernelILb1ELb0E"])
 def test_mickey_clock_loop_is_straight_line_lop3(kernel):
     kernels = _kernel_sass(kernel)
     assert kernels, f"{kernel} not found in libmk2.so"
@@ -67,8 +67,8 @@ def test_mickey_clock_loop_is_straight_line_lop3(kernel):
 
 
 @pytest.mark.parametrize("kernel,which", [("mk219gen_colmajor_kernel", 0),
-                                          ("mk219gen_rowmajor_kernelILb1ELi32ELi224E", 1),
-                                          ("mk24tmem19gen_rowmajor_kernelILb1E", 1),
+                                          ("mk219gen_rowmajor_kernelILb1ELi32ELi224ELb0E", 1),
+                                          ("mk24tmem19gen_rowmajor_kernelILb1ELb0E", 1),
                                           ("mk211init_kernelILb0E", 2)])
 def test_blocked_clock_loop_matches_the_predicted_lop3_count(kernel, which):
     lib = _native.lib()
@@ -95,7 +95,7 @@ def test_blocked_clock_loop_matches_the_predicted_lop3_count(kernel, which):
 def test_tensor_memory_kernel_uses_tcgen05_and_no_shared_memory_tile():
     """The default row-major kernel stages keystream in tensor memory: STTM / LDTM in the SASS, the allocation
     (UTCATOMSWS) at entry, and no shared-memory loads or stores in its loops."""
-    (name, ins), = _kernel_sass("mk24tmem19gen_rowmajor_kernelILb1E").items()
+    (name, ins), = _kernel_sass("mk24tmem19gen_rowmajor_kernelILb1ELb0E").items()
     texts = [t for _, t in ins]
     assert sum(t.startswith("STTM") for t in texts) >= 6 and sum(t.startswith("LDTM") for t in texts) >= 17
     assert any("UTCATOMSWS" in t for t in texts)
@@ -113,3 +113,15 @@ def test_init_and_grain_loops_have_no_spills_or_branches():
             texts = [t for _, t in min(loops, key=len)]
             assert not [t for t in texts if re.search(r"\b(LDL|STL)\b", t)], name
             assert sum(bool(re.match(r"(@!?U?P\d+\s+)?BRA", t)) for t in texts) == 1, name
+
+
+def test_ragged_init_holds_late_lanes_with_five_extra_lop3_per_clock():
+    """init_kernel<RAGGED>: the IV phase of a group with per-lane IV lengths runs masked 4-clock blocks
+    (clock_block_masked, csrc/mk2_clock.cuh): the load block's LOP3 count plus 5 per clock (the COMP0 & COMP1
+    positions without a feedback XOR to fold the mask into), not 200 ANDs per clock."""
+    lib = _native.lib()
+    K, predicted = lib.mk2_rblock(2), lib.mk2_lop3_per_block(2)
+    (name, ins), = _kernel_sass("mk211init_kernelILb1E").items()
+    counts = sorted(sum("LOP3" in t for _, t in body) for body in _innermost_clock_loops(ins, predicted - 2, predicted + 40))
+    assert len(counts) >= 3, counts                      # pre-clock blocks, load blocks, masked load blocks
+    assert predicted + 5 * K <= counts[-1] <= predicted + 5 * K + 14, (counts, predicted)
