@@ -2,14 +2,20 @@
 """bench.py -- keystream Tb/s of the bitsliced MICKEY 2.0 path on N B200s.
 
     python bench.py --gpus N --steps K --warmup W            (our CUDA path)
-    python bench.py --impl reference --gpus N --steps K ...  (CPU arm: oracle port)
+    python bench.py --impl reference --gpus N --steps K ...  (CPU arm: the reference's numba loop, else the oracle port)
 
 A step = one pass of the hot path over one batch of synthetic key/IV material:
-device-side counter-IV synthesis, key/IV load + 100 pre-clocks, the keystream
-loop and the stores.  Default workload = BASELINE.json configs[1]:
-2^20 instances x 1 Mbit per GPU, column-major output resident in HBM (131 GB,
->> L2, so no L2 flush is needed between steps).  With N > 1 every rank takes a
-disjoint key/IV (instance-index) range of the same size: weak scaling, no
+device-side counter-IV synthesis (or explicit key/IV arrays), key/IV load + 100
+pre-clocks, the keystream loop and the stores.  Headline workload = BASELINE.json
+configs[1] ("c2"): 2^20 instances x 1 Mbit per GPU, column-major output resident
+in HBM (131 GB, >> L2, so no L2 flush is needed between steps).  The same run
+also measures configs[2] ("c3", 2^24 x 64 Kbit row-major) and configs[4] ("c5",
+2^26 fresh key/IV pairs x 1 Kbit) as `extra_workloads`, each with its own
+roofline record, and the host-buffer legs `e2e` (pinned) and `e2e_pageable`.
+
+Multi-GPU (one process per GPU under torchrun): `--scaling weak` gives every rank
+its own disjoint key/IV range of the workload's size; `--scaling strong
+--total-bits B` splits B bits (configs[3]: 8e12 = 1 TB) over the ranks.  No
 data-path collective; one 8-byte checksum all-reduce after the timed region.
 
 Prints ONE JSON line on rank 0 (see DESIGN.md "Measurement" for every field).
@@ -32,11 +38,24 @@ sys.path.insert(0, str(ROOT))
 KEY = bytes.fromhex("123456789abcdef01234")  # eSTREAM vector key (vectors.py:42)
 METRIC = "keystream Tb/s, bitsliced MICKEY 2.0"
 LOP3_PER_CLOCK_SURVEY = 327  # LOP3 per clock per 32-lane word, one clock at a time
-# dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the dominant kernel, from the committed
-# `ncu --set full` captures (per launch, like roofline.achieved); only for launches captured exactly.
+# dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the dominant kernel from the committed
+# `ncu --set full` captures.  NOT measured in this run: quoted (with its source file) only for a launch of exactly
+# this geometry, next to `traffic_model`, which IS computed in the run from the launch plan.
 NCU_TRAFFIC = {
     # (layout, instances, clocks): (bytes, source)
     ("colmajor", 1 << 20, 1_000_000): (131_438_553_000 + 512_053_248, "profiles/r01b_ncu_gen_colmajor_c2_full_1Mclk.txt"),
+}
+try:  # captures added later in the round register themselves here (profiles/ncu_traffic.json)
+    for _k, _v in json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).items():
+        _layout, _n, _t = _k.split(":")
+        NCU_TRAFFIC[(_layout, int(_n), int(_t))] = (int(_v["bytes"]), _v["source"])
+except (OSError, ValueError, KeyError):
+    pass
+
+WORKLOADS = {  # name -> (instances log2, clocks, layout, BASELINE.json config index)
+    "c2": (20, 1_000_000, "colmajor", 1),
+    "c3": (24, 65_536, "rowmajor", 2),
+    "c5": (26, 1_024, "rowmajor", 4),
 }
 
 
@@ -46,33 +65,27 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("c2", "c3", "c5"), default="c2",
-                    help="c2: 2^20 x 1 Mbit column-major (default, BASELINE configs[1]); "
-                         "c3: 2^24 x 64 Kbit row-major; c5: 2^26 x 1 Kbit init-dominated")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c2",
+                    help="headline workload: c2 2^20 x 1 Mbit column-major (default, BASELINE configs[1]); "
+                         "c3 2^24 x 64 Kbit row-major; c5 2^26 x 1 Kbit init-dominated")
+    ap.add_argument("--extras", default="auto",
+                    help="other single-GPU configs measured in the same run as extra_workloads: 'auto' (the other two "
+                         "at N=1 with the default workload), 'none', or a comma list of c2,c3,c5")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
+    ap.add_argument("--total-bits", type=float, default=8e12,
+                    help="strong scaling: keystream bits of the whole job (BASELINE configs[3]: 1 TB = 8e12)")
     ap.add_argument("--instances-log2", type=int, default=None, help="override instances per GPU (log2)")
     ap.add_argument("--clocks", type=int, default=None, help="override keystream bits per instance")
-    ap.add_argument("--e2e-clocks", type=int, default=16384, help="keystream bits per instance of one e2e step")
+    ap.add_argument("--e2e-clocks", type=int, default=16384, help="keystream bits per instance of one host-output call")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-curand", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target size of the CPU sample")
+    ap.add_argument("--cpu-kind", choices=("auto", "reference", "port"), default="auto",
+                    help="--impl reference: the reference's own numba loop from oracle/_ref (auto: when importable), "
+                         "or the oracle's C port")
     return ap.parse_args()
-
-
-WORKLOADS = {  # name -> (instances log2, clocks, layout)
-    "c2": (20, 1_000_000, "colmajor"),
-    "c3": (24, 65_536, "rowmajor"),
-    "c5": (26, 1_024, "rowmajor"),
-}
-
-
-def workload_of(args):
-    lg, clocks, layout = WORKLOADS[args.workload]
-    if args.instances_log2 is not None:
-        lg = args.instances_log2
-    if args.clocks is not None:
-        clocks = args.clocks
-    return 1 << lg, clocks, layout
 
 
 # ----------------------------------------------------------------------------- clocks sampler
@@ -159,26 +172,94 @@ def cpu_sample(seconds: float, threads: int | None = None) -> dict:
                       f"(oracle/mickey_oracle.c port of kernels.py:46-95, gcc -O3 -march=x86-64-v3)"}
 
 
+def reference_import():
+    """The UNMODIFIED reference package staged under oracle/_ref by oracle/stage_ref.py (git-ignored; travels to
+    the GPU box with the tree).  Returns (slicerng.bench module, None) or (None, reason)."""
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "slicerng" / "bench.py").exists():
+        return None, "oracle/_ref/slicerng is not staged (run python oracle/stage_ref.py where /root/reference exists)"
+    cache = Path(os.environ.get("NUMBA_CACHE_DIR") or "/tmp/mk2_numba_cache")   # kernels.py:27 uses cache=True
+    cache.mkdir(parents=True, exist_ok=True)
+    os.environ["NUMBA_CACHE_DIR"] = str(cache)
+    sys.path.insert(0, str(ref))
+    try:
+        import slicerng.bench as rb
+        return rb, None
+    except Exception as exc:  # numba missing, import error ...
+        sys.path.remove(str(ref))
+        return None, f"import of oracle/_ref/slicerng failed: {exc!r}"
+
+
+def reference_sample(rb, workers: int, mib_per_worker: int, repeats: int = 3) -> dict:
+    """One bench.measure("mickey", "sliced", ...) of the reference itself (bench.py:228-283): its numba
+    _mickey_sliced_loop (kernels.py:46-95), W=64, `workers` threads (the kernels are nogil), median of repeats."""
+    nbytes = workers * (mib_per_worker << 20)
+    t0 = time.perf_counter()
+    res = rb.measure("mickey", "sliced", nbytes=nbytes, warmup=1, repeats=max(repeats, rb.MIN_REPEATS), workers=workers)
+    wall = time.perf_counter() - t0
+    med = statistics.median(res.runs) if hasattr(res, "runs") else res.seconds
+    return {"value": res.nbytes * 8 / med / 1e12, "unit": "Tb/s", "cores": workers, "kind": "reference",
+            "seconds": round(wall, 3), "median_run_s": med, "bytes": res.nbytes,
+            "sample": f"slicerng.bench.measure('mickey','sliced', nbytes={res.nbytes}, repeats={len(getattr(res, 'runs', ()))}, "
+                      f"workers={workers}): the reference's own numba loop (kernels.py:46-95), W=64, median of repeats; "
+                      f"with workers > 1 its timed region includes each worker's pure-Python init (bench.py:265-282)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n, clocks, layout = workload_of(args)
-    per_step = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_sample(min(per_step, 2.0))
-    vals = [cpu_sample(per_step) for _ in range(args.steps)]
-    dt = sum(v["seconds"] for v in vals)
-    bits = sum(v["value"] * 1e12 * v["seconds"] for v in vals)
-    value = bits / dt / 1e12
+    lg, clocks, layout, _cfg = WORKLOADS[args.workload]
+    n = 1 << (args.instances_log2 or lg)
+    clocks = args.clocks or clocks
+    cores = os.cpu_count() or 1
+    rb, why = (None, "--cpu-kind port") if args.cpu_kind == "port" else reference_import()
+    if rb is None and args.cpu_kind == "reference":
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return
+    budget = 150.0  # seconds for the whole arm
+    if rb is not None:
+        try:
+            one = reference_sample(rb, 1, 64)                              # bench.measure(..., workers=1): BASELINE.md 4
+            # size the all-core sample from the one-worker rate: about budget / (steps + warmup) seconds per step
+            per_step = max(4.0, min(20.0, budget / max(1, args.steps + args.warmup)))
+            rate = one["bytes"] / one["median_run_s"]                      # bytes/s of one worker
+            mib = int(max(8, min(256, rate * per_step / 3 / (1 << 20))))   # 3 repeats per measure()
+            for _ in range(min(args.warmup, 1)):
+                reference_sample(rb, cores, max(8, mib // 4))
+            vals = [reference_sample(rb, cores, mib) for _ in range(args.steps)]
+            extra = {"one_thread_gbit_s": one["value"] * 1e3}
+            try:
+                naive = rb.measure("mickey", "naive", nbytes=rb.MIN_BYTES, repeats=rb.MIN_REPEATS)
+                extra["naive_one_thread_gbit_s"] = naive.nbytes * 8 / statistics.median(naive.runs) / 1e9
+            except Exception:
+                pass
+        except Exception as exc:
+            rb, why = None, f"slicerng.bench.measure failed: {exc!r}"
+    if rb is None:
+        per_step = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
+        for _ in range(args.warmup):
+            cpu_sample(min(per_step, 2.0))
+        vals = [cpu_sample(per_step) for _ in range(args.steps)]
+        extra = {k: vals[-1][k] for k in ("one_thread_gbit_s", "naive_one_thread_gbit_s")}
+        extra["reference_unavailable"] = why
+    if vals[0]["kind"] == "reference":
+        # every measure() call is one step: its value is the median-of-repeats rate the reference reports
+        value = statistics.median(v["value"] for v in vals)
+        ms_per_step = statistics.median(v["median_run_s"] for v in vals) * 1e3
+    else:
+        dt = sum(v["seconds"] for v in vals)
+        value = sum(v["value"] * v["seconds"] for v in vals) / dt
+        ms_per_step = dt / args.steps * 1e3
     last = vals[-1]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Tb/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: 2^{n.bit_length() - 1} instances x {clocks} bits per GPU, {layout} "
                                f"(CPU arm: bounded sample of the same keystream loop)"},
-        "cpu_baseline": {**{k: last[k] for k in ("unit", "cores", "kind", "sample", "one_thread_gbit_s", "naive_one_thread_gbit_s")}, "value": value},
+        "cpu_baseline": {"value": value, "unit": "Tb/s", "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"], **extra},
         "e2e": {"value": value, "unit": "Tb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -215,47 +296,79 @@ def curand_compare(torch, nbytes: int) -> dict:
     return out
 
 
-def run_ours(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
+class Env:
+    """Process-wide context of the GPU arm: torch, ranks, the one context (generator) of this rank."""
 
-    import paper_1909_04750_b200 as pkg
-    from paper_1909_04750_b200 import sharding
+    def __init__(self, args):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device; the MICKEY path has no CPU fallback")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import paper_1909_04750_b200 as pkg
+        from paper_1909_04750_b200 import _native
 
-    def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
-        torch.cuda.synchronize()
+        self.args, self.np, self.torch, self.dist, self.pkg = args, np, torch, dist, pkg
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py: no CUDA device; the MICKEY path has no CPU fallback")
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.stream = torch.cuda.current_stream()
+        self.lib = _native.lib()
+        self.gen = pkg.MickeyGenerator(self.local)
+        self.gen.set_stream(self.stream.cuda_stream)
+        self.gen.set_async(True)               # we time the stream ourselves
+        self.peaks, self.peaks_src = measured_peaks()
+        self.lop3_peak = None
 
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier(device_ids=[self.local])
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
-    n, clocks, layout = workload_of(args)
+    def gather_rows(self, row):
+        """One small float64/int64 row per rank -> list of rows on every rank (after the timed region)."""
+        torch = self.torch
+        t = torch.tensor(row, dtype=torch.int64, device=self.dev)
+        if self.world == 1:
+            return [t.tolist()]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t)
+        return [o.tolist() for o in out]
+
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def peak(self):
+        if self.lop3_peak is None:
+            self.gen.set_async(False)
+            self.lop3_peak, _ = self.gen.lop3_peak()
+            self.gen.set_async(True)
+        return self.lop3_peak
+
+
+def measure_workload(env: Env, name: str, n: int, clocks: int, layout: str, first: int, steps: int, warmup: int,
+                     stride_per_step: int, sampler: ClockSampler | None = None) -> dict:
+    """W warm-up + K timed steps of one workload on this rank.  Returns the per-workload record (rank-local
+    kernel figures; `elapsed_ms` is the max over ranks)."""
+    torch, gen, stream = env.torch, env.gen, env.stream
     G = n // 32
-    first = rank * n                       # disjoint key/IV (instance index) range per rank
-    stream = torch.cuda.current_stream()
-    gen = pkg.MickeyGenerator(local)
-    gen.set_stream(stream.cuda_stream)
-    gen.set_async(True)                    # we time the stream ourselves
     gen.set_group_offset(first // 32)
 
     # ---- output buffer: whole keystream of one step resident in HBM when it fits
     out_bytes = n * clocks // 8
+    torch.cuda.empty_cache()
     free, _total = torch.cuda.mem_get_info()
     state_bytes = G * (800 + 8 + 640) + (1 << 30)
     if out_bytes + state_bytes <= free:
@@ -265,34 +378,39 @@ def run_ours(args):
         chunk_clocks = max(1024, budget * 8 // n // 1024 * 1024)
         out_mode = f"ring({chunk_clocks} clocks)"
     if layout == "colmajor":
-        out = torch.empty((chunk_clocks, G), dtype=torch.int32, device=dev)
+        out = torch.empty((chunk_clocks, G), dtype=torch.int32, device=env.dev)
     else:
-        out = torch.empty((n, chunk_clocks // 8), dtype=torch.uint8, device=dev)
-
-    ev = lambda: torch.cuda.Event(enable_timing=True)
-    gen_events = []
-    launches = 0
+        out = torch.empty((n, chunk_clocks // 8), dtype=torch.uint8, device=env.dev)
 
     # c5 (fresh key/IV pairs, init-dominated): explicit material arrays resident in HBM, so that the row-major
     # key/IV bytes -> bitsliced input words transposition is part of the step; c2 / c3: the
     # counter-IV set synthesised on device
-    explicit = args.workload == "c5"
+    explicit = name == "c5"
     if explicit:
-        gsrc = torch.Generator(device=dev).manual_seed(0x190904750 + rank)
-        d_keys = torch.randint(0, 256, (n, 10), dtype=torch.uint8, device=dev, generator=gsrc)
-        d_ivs = torch.randint(0, 256, (n, 10), dtype=torch.uint8, device=dev, generator=gsrc)
+        gsrc = torch.Generator(device=env.dev).manual_seed(0x190904750 + env.rank)
+        d_keys = torch.randint(0, 256, (n, 10), dtype=torch.uint8, device=env.dev, generator=gsrc)
+        d_ivs = torch.randint(0, 256, (n, 10), dtype=torch.uint8, device=env.dev, generator=gsrc)
+
+    gen_events, init_events = [], []
+    launches = 0
+    plan = None
 
     def step(i: int, record: bool):
-        nonlocal launches
+        nonlocal launches, plan
+        e0, e1 = env.event(), env.event()
+        e0.record(stream)
         if explicit:
             gen.init_material(d_keys, d_ivs, 80)
         else:
-            gen.init_counter(KEY, first + (i % 4) * world * n, n)
+            gen.init_counter(KEY, first + (i % 4) * stride_per_step, n)
+        e1.record(stream)
         launches += gen.last_kernel_launches
+        if record:
+            init_events.append((e0, e1))
         done = 0
         while done < clocks:
             tc = min(chunk_clocks, clocks - done)
-            e0, e1 = ev(), ev()
+            e0, e1 = env.event(), env.event()
             e0.record(stream)
             if layout == "colmajor":
                 gen.generate_colmajor(tc, out)
@@ -302,54 +420,57 @@ def run_ours(args):
             launches += gen.last_kernel_launches
             if record:
                 gen_events.append((e0, e1, tc))
+            if plan is None:
+                plan = gen.last_plan()
             done += tc
 
-    for i in range(args.warmup):
+    for i in range(warmup):
         step(i, False)
-    barrier()
-    sampler = ClockSampler(local)
-    if rank == 0:
+    env.barrier()
+    if sampler is not None:
         sampler.start()
         time.sleep(0.25)
     launches = 0
     t_wall0 = time.perf_counter()
-    start, end = ev(), ev()
-    barrier()
+    start, end = env.event(), env.event()
+    env.barrier()
     start.record(stream)
-    for i in range(args.steps):
-        step(args.warmup + i, True)
+    for i in range(steps):
+        step(warmup + i, True)
     end.record(stream)
-    barrier()
+    env.barrier()
     t_wall1 = time.perf_counter()
-    clocks_info = sampler.stop(t_wall0, t_wall1) if rank == 0 else None
-    elapsed_ms = max_over_ranks(start.elapsed_time(end))
+    clocks_info = sampler.stop(t_wall0, t_wall1) if sampler is not None else None
+    local_ms = start.elapsed_time(end)
+    elapsed_ms = env.max_over_ranks(local_ms)
     gen_ms = [e0.elapsed_time(e1) for e0, e1, _ in gen_events]
+    init_ms = [e0.elapsed_time(e1) for e0, e1 in init_events]
     gen_clk = sum(tc for _, _, tc in gen_events)
     kernel_ms_total = sum(gen_ms)
-    timed_launches = launches
+    checksum = gen.checksum()                          # of the last step's keystream, this rank's range
 
-    bits_per_step = world * n * clocks
-    value = bits_per_step * args.steps / (elapsed_ms * 1e-3) / 1e12
-
-    # ---- checksum: the only exchange (8 bytes, NCCL sum), outside the timed region
-    csum = sharding.allreduce_checksum(gen.checksum(), device=dev)
-
-    # ---- roofline of the dominant kernel (keystream loop), this rank
-    peaks, peaks_src = measured_peaks()
-    gen.set_async(False)
-    lop3_peak, _ = gen.lop3_peak()
-    # Algorithmic LOP3 per clock of the kernel as built: the clock runs in blocks of K clocks with R's
-    # reduction deferred (csrc/mk2_clock.cuh); mk2_lop3_per_block is derived from the cipher's tables and
-    # checked against the SASS by tests/test_structure.py.  SURVEY.md 8(d) counted 327 for the one-clock form.
+    # ---- roofline of the dominant kernel (keystream loop), this rank.
+    # Algorithmic LOP3 per clock of the kernel as built: the clock runs in blocks of K clocks with R's reduction
+    # deferred (csrc/mk2_clock.cuh); mk2_lop3_per_block is derived from the cipher's tables and checked against
+    # the SASS by tests/test_structure.py.  SURVEY.md 8(d) counted 327 for the one-clock form.
+    lib = env.lib
     which = 0 if layout == "colmajor" else 1
-    from paper_1909_04750_b200 import _native
-    lib = _native.lib()
     rblock, per_block = lib.mk2_rblock(which), lib.mk2_lop3_per_block(which)
     lop3_per_clock = per_block / rblock
+    lop3_peak = env.peak()
     lane_ops = n * gen_clk * lop3_per_clock / 32          # algorithmic LOP3 lane-ops in the timed launches
     achieved = lane_ops / (kernel_ms_total * 1e-3)
     achieved_survey = achieved * LOP3_PER_CLOCK_SURVEY / lop3_per_clock
     hbm_gbs = (n * gen_clk / 8) / (kernel_ms_total * 1e-3) / 1e9
+    launch_clocks = gen_events[0][2] if gen_events else 0
+    # in-run traffic model of one launch: the stores of the keystream itself plus the state parking of the
+    # persistent scheduler (every chain-chunk job loads and stores 200 state words + one 8-byte accumulator per
+    # thread, through L2); everything else (scheduler ring, progress words) is below 1 MB
+    block_threads, chunk = plan if plan else (0, 0)
+    jobs = ((n + 1023) // 1024) * (-(-launch_clocks // chunk) if chunk else 0)
+    traffic_model = n * launch_clocks // 8 + jobs * 32 * 2 * (800 + 8)
+    ncu_bytes, ncu_src = NCU_TRAFFIC.get((layout, n, launch_clocks), (None, None))
+    peaks = env.peaks
     roofline = {
         "bound": "lop3", "kernel": "gen_colmajor_kernel" if layout == "colmajor" else "tmem::gen_rowmajor_kernel",
         "achieved": achieved / 1e12, "peak": lop3_peak / 1e12, "unit": "Tlane-op/s", "frac": achieved / lop3_peak,
@@ -361,41 +482,170 @@ def run_ours(args):
                             "note": "same run priced at SURVEY 8(d)'s 327 LOP3 per clock: above 1 because the "
                                     "deferred R reduction executes fewer LOP3 than the one-clock form"},
         "avg_launch_ms": kernel_ms_total / max(1, len(gen_events)),
-        "kernel_share_of_step": kernel_ms_total / start.elapsed_time(end),
-        "traffic": NCU_TRAFFIC.get((layout, n, gen_events[0][2] if gen_events else 0), (None, None))[0],
-        "traffic_source": NCU_TRAFFIC.get((layout, n, gen_events[0][2] if gen_events else 0), (None, None))[1],
-        "algorithmic_bytes_per_launch": n * (gen_events[0][2] if gen_events else 0) // 8,
+        "kernel_share_of_step": kernel_ms_total / local_ms,
+        "plan": {"threads_per_cta": block_threads, "chunk_clocks": chunk, "jobs_per_launch": jobs},
+        "traffic": ncu_bytes,
+        "traffic_source": (f"{ncu_src}: ncu --set full capture of a launch of exactly this geometry, committed earlier; "
+                           f"NOT measured in this run") if ncu_src else None,
+        "traffic_model": traffic_model,
+        "traffic_model_source": "computed in this run from the launch plan: keystream stores + state parking of every "
+                                "chain-chunk job (2 x 808 B per thread)",
+        "algorithmic_bytes_per_launch": n * launch_clocks // 8,
         "hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": hbm_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
-                "peak_source": f"MEASURED_PEAKS.json ({peaks_src})", "note": "0.125 B stored per keystream bit; not binding"},
+                "peak_source": f"MEASURED_PEAKS.json ({env.peaks_src})", "note": "0.125 B stored per keystream bit; not binding"},
+    }
+    # whole step (pack + key/IV load + pre-clocks + keystream) against the same LOP3 peak: 160 load clocks and
+    # 100 pre-clocks per instance at the init kernel's block count, T keystream clocks at the keystream kernel's
+    irb, ipb = lib.mk2_rblock(2), lib.mk2_lop3_per_block(2)
+    step_ops = n / 32 * ((160 + 100) * ipb / irb + clocks * lop3_per_clock) * steps
+    split = {
+        "init_ms_per_step": sum(init_ms) / max(1, steps), "keystream_ms_per_step": kernel_ms_total / max(1, steps),
+        "init_note": ("pack_uniform_kernel (u8[N][10] key / IV rows -> bitsliced input words) + init_kernel" if explicit
+                      else "pack_counter_kernel + init_kernel") + ": 160 load clocks + 100 pre-clocks per instance",
+        "whole_step_lop3_frac": step_ops / (local_ms * 1e-3) / lop3_peak,
+        "init_kernel_lop3_frac": (n / 32 * 260 * ipb / irb * steps) / (sum(init_ms) * 1e-3) / lop3_peak if init_ms else None,
+    }
+    del out
+    if explicit:
+        del d_keys, d_ivs
+    torch.cuda.empty_cache()
+    return {
+        "name": name, "n": n, "clocks": clocks, "layout": layout, "explicit": explicit, "out_mode": out_mode,
+        "out_bytes": out_bytes, "steps": steps, "warmup": warmup, "elapsed_ms": elapsed_ms, "local_ms": local_ms,
+        "launches": launches, "roofline": roofline, "split": split, "clocks_info": clocks_info, "checksum": checksum,
+        "first": first,
     }
 
-    # ---- e2e: host key/IV arrays in, host keystream out, through the public API
-    e2e = None
+
+def workload_text(name, n, clocks, layout, explicit):
+    return (f"{name}: 2^{n.bit_length() - 1} instances x {clocks} bits per GPU, {layout}, "
+            + ("explicit key/IV arrays (u8[N][10] each) resident in HBM, " if explicit else
+               "counter-IV material synthesised on device, ") + "init + keystream per step") if n & (n - 1) == 0 else \
+           (f"{name}: {n} instances x {clocks} bits per GPU, {layout}, counter-IV material synthesised on device, "
+            "init + keystream per step")
+
+
+def checksum_crosscheck(env: Env, shards) -> dict:
+    """The only collective of the path, checked in the run: every rank computes the checksum of a small slice of
+    ITS key/IV range (first 2048 instances x 512 bits) and the values are summed with one all-reduce (NCCL);
+    rank 0 then recomputes every slice alone on its own GPU and must get the same 64-bit sum."""
+    from paper_1909_04750_b200 import sharding
+
+    pkg = env.pkg
+    T = 512
+
+    def slice_sum(first, count):
+        with pkg.MickeyGenerator(env.local) as g:
+            g.set_group_offset(first // 32)
+            g.init_counter(KEY, first, min(count, 2048))
+            g.generate_colmajor(T, env.torch.empty((T, (min(count, 2048) + 31) // 32), dtype=env.torch.int32, device=env.dev))
+            return g.checksum()
+
+    first, count = shards[env.rank]
+    mine = slice_sum(first, count)
+    reduced = sharding.allreduce_checksum(mine, device=env.dev)
+    alone = 0
+    if env.rank == 0:
+        for f, c in shards:
+            alone = (alone + slice_sum(f, c)) % (1 << 64)
+    return {"slice": f"first {min(count, 2048)} instances of every rank x {T} bits", "allreduced": f"{reduced:#018x}",
+            "single_rank_recomputation": f"{alone:#018x}", "equal": reduced == alone if env.rank == 0 else None,
+            "collective": "one int64 SUM all-reduce (NCCL)" if env.world > 1 else "none (world size 1)"}
+
+
+def run_ours(args):
+    env = Env(args)
+    np, torch, pkg, gen = env.np, env.torch, env.pkg, env.gen
+    from paper_1909_04750_b200 import sharding
+
+    world, rank, local = env.world, env.rank, env.local
+    lg, clocks, layout, cfg = WORKLOADS[args.workload]
+    if args.instances_log2 is not None:
+        lg = args.instances_log2
+    if args.clocks is not None:
+        clocks = args.clocks
+    if args.scaling == "strong":
+        # configs[3]: a fixed job of total_bits, split into disjoint contiguous key/IV ranges of whole groups
+        total_n = max(32 * world, int(args.total_bits // clocks) // 32 * 32)
+        sh = sharding.shard_instances(total_n, world, rank)
+        n, first, stride = sh.count, sh.first, total_n
+        shards = [(s.first, s.count) for s in (sharding.shard_instances(total_n, world, r) for r in range(world))]
+    else:
+        n = 1 << lg
+        first, stride, total_n = rank * n, world * n, world * n   # disjoint key/IV (instance index) range per rank
+        shards = [(r * n, n) for r in range(world)]
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    main = measure_workload(env, args.workload, n, clocks, layout, first, args.steps, args.warmup, stride, sampler)
+    bits_per_step = total_n * clocks
+    value = bits_per_step * args.steps / (main["elapsed_ms"] * 1e-3) / 1e12
+
+    # ---- per-rank record + the checksum all-reduce (the only exchange; outside the timed region)
+    csum = sharding.allreduce_checksum(main["checksum"], device=env.dev)
+    rows = env.gather_rows([rank, first, n, int(round(main["local_ms"] * 1e3)), sharding.to_i64(main["checksum"])])
+    ranks = [{"rank": r[0], "first": r[1], "count": r[2], "ms": r[3] / 1e3, "checksum": f"{sharding.from_i64(r[4]):#018x}"}
+             for r in rows]
+    check = checksum_crosscheck(env, shards)
+
+    # ---- the other single-GPU configs of BASELINE.json, same process, same protocol
+    extras = {}
+    if args.extras == "auto":
+        extra_names = [w for w in WORKLOADS if w != args.workload] if (world == 1 and args.workload == "c2"
+                                                                      and args.scaling == "weak"
+                                                                      and args.instances_log2 is None
+                                                                      and args.clocks is None) else []
+    elif args.extras == "none":
+        extra_names = []
+    else:
+        extra_names = [w for w in args.extras.split(",") if w in WORKLOADS and w != args.workload]
+    for w in extra_names:
+        wlg, wclk, wlay, wcfg = WORKLOADS[w]
+        wn = 1 << wlg
+        k = max(1, min(args.steps, 5))
+        rec = measure_workload(env, w, wn, wclk, wlay, rank * wn, k, max(3, min(args.warmup, 3)), world * wn)
+        extras[w] = {
+            "baseline_config": f"BASELINE.json configs[{wcfg}]",
+            "workload": workload_text(w, wn, wclk, wlay, rec["explicit"]),
+            "value": world * wn * wclk * k / (rec["elapsed_ms"] * 1e-3) / 1e12, "unit": "Tb/s",
+            "ms_per_step": rec["elapsed_ms"] / k, "steps": k, "warmup": rec["warmup"], "output": rec["out_mode"],
+            "gpu_launches": rec["launches"], "roofline": rec["roofline"], "step_split": rec["split"],
+            "checksum_u64_sum": f"{rec['checksum']:#018x}",
+        }
+
+    # ---- host-buffer legs through the public API
+    e2e = e2e_page = latency = None
     if not args.no_e2e:
-        del out
-        torch.cuda.empty_cache()
-        e2e = run_e2e(args, torch, np, pkg, gen, n, clocks, layout, first, world, barrier, max_over_ranks)
+        e2e, e2e_page = run_e2e(env, n, clocks, layout, first)
+    if not args.no_latency and rank == 0:
+        latency = small_call_latency(env)
 
     line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Tb/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": main["elapsed_ms"] / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {
-                "workload": f"{args.workload}: 2^{n.bit_length() - 1} instances x {clocks} bits per GPU, {layout}, "
-                            + ("explicit key/IV arrays (u8[N][10] each) resident in HBM, " if explicit else
-                               "counter-IV material synthesised on device, ") + "init + keystream per step",
-                "instances_per_gpu": n, "clocks": clocks, "layout": layout, "output": out_mode,
-                "l2": f"no flush needed: each step streams {out_bytes / 1e9:.1f} GB of output per GPU (>> 126 MB L2)",
-                "parallelism": f"{world} x disjoint key/IV ranges, no data-path collective",
+                "workload": workload_text(args.workload, n, clocks, layout, main["explicit"]),
+                "baseline_config": f"BASELINE.json configs[{cfg}]" + (" shape per rank; configs[3] job" if args.scaling == "strong" else ""),
+                "instances_per_gpu": n, "clocks": clocks, "layout": layout, "output": main["out_mode"],
+                "total_instances": total_n, "total_bits_per_step": bits_per_step,
+                "l2": f"no flush needed: each step streams {main['out_bytes'] / 1e9:.1f} GB of output per GPU (>> 126 MB L2)",
+                "parallelism": f"{world} x disjoint key/IV ranges ({args.scaling} scaling), no data-path collective",
             },
-            "roofline": roofline, "clocks": clocks_info, "gpu_launches": timed_launches,
-            "checksum_u64_sum": f"{csum:#018x}",
+            "roofline": main["roofline"], "step_split": main["split"], "clocks": main["clocks_info"],
+            "gpu_launches": main["launches"],
+            "checksum_u64_sum": f"{csum:#018x}", "ranks": ranks, "checksum_check": check,
         }
+        if extras:
+            line["extra_workloads"] = extras
         if e2e:
             line["e2e"] = e2e
+        if e2e_page:
+            line["e2e_pageable"] = e2e_page
+        if latency:
+            line["small_call_latency"] = latency
         if not args.no_curand:
             try:
                 line["curand"] = curand_compare(torch, 1 << 32)
@@ -405,56 +655,166 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_sample(args.cpu_seconds)
     gen.close()
     if world > 1:
-        dist.barrier(device_ids=[local])
-        dist.destroy_process_group()
+        env.dist.barrier(device_ids=[local])
+        env.dist.destroy_process_group()
     if line:
         print(json.dumps(line), flush=True)
 
 
-def run_e2e(args, torch, np, pkg, gen, n, clocks, layout, first, world, barrier, max_over_ranks):
-    """Same metric through the C-ABI call with HOST buffers: pinned key/IV
-    arrays in (H2D inside the call), pinned keystream buffer out (D2H inside)."""
-    # bounded sample of the same workload: <= 2 GiB of keystream per step (the link bounds e2e, not the kernel)
-    tc = min(args.e2e_clocks, clocks // 8 * 8)
+def run_e2e(env: Env, n, clocks, layout, first):
+    """Same metric through the C-ABI call with HOST buffers, host<->device copies inside the timed region.
+      e2e           pinned key/IV arrays in, pinned keystream out, the WHOLE workload length: column-major runs
+                    the full `clocks` as resumable calls of --e2e-clocks bits into a ring of two pinned buffers
+                    (the consumer owns one while the next fills); row-major is the one-shot mk2_bulk_rowmajor.
+      e2e_pageable  the reference's calling convention (kernels.py:189-200): ordinary (pageable) numpy key/IV
+                    arrays in, numpy keystream out -- into a caller-supplied pageable array (pinned bounce tiles
+                    + copy workers inside the library) and into the fresh result array the package returns
+                    (page-locked block from its pool).  Bounded sample: one --e2e-clocks call per step."""
+    args, np, torch, pkg, gen = env.args, env.np, env.torch, env.pkg, env.gen
+    world = env.world
+    tc = max(8, min(args.e2e_clocks, clocks) // 8 * 8)
     n_full = n
-    n = max(1024, min(n, (1 << 34) // tc // 1024 * 1024))
-    keys = torch.from_numpy(np.tile(np.frombuffer(KEY, np.uint8), (n, 1))).pin_memory()
+    n = max(1024, min(n, (1 << 34) // tc // 1024 * 1024))      # <= 2 GiB of keystream per call
+    keys_np = np.tile(np.frombuffer(KEY, np.uint8), (n, 1))
     idx = (np.arange(n, dtype=np.uint64) + np.uint64(first))
     ivs_np = np.zeros((n, 10), np.uint8)
     ivs_np[:, 2:] = idx.astype(">u8").view(np.uint8).reshape(n, 8)   # 80-bit big-endian index
-    ivs = torch.from_numpy(ivs_np).pin_memory()
-    if layout == "colmajor":
-        host = torch.empty((tc, n // 32), dtype=torch.int32).pin_memory()
-    else:
-        host = torch.empty((n, tc // 8), dtype=torch.uint8).pin_memory()
+    keys, ivs = torch.from_numpy(keys_np).pin_memory(), torch.from_numpy(ivs_np).pin_memory()
     gen.set_stream(None)
     gen.set_async(False)
+    steps = max(1, min(args.steps, 3))
+    G = n // 32
 
-    def one():
-        if layout == "colmajor":
+    def timed(fn, reps, warm=1):
+        for _ in range(warm):
+            fn()
+        env.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return env.max_over_ranks(time.perf_counter() - t0) / reps
+
+    # ---- pinned, whole length
+    if layout == "colmajor":
+        ring = [torch.empty((tc, G), dtype=torch.int32).pin_memory() for _ in range(2)]
+        full_clocks = clocks if n == n_full else tc
+        ncalls = -(-full_clocks // tc)
+
+        def one():
             gen.init_material(keys, ivs, 80)
-            gen.generate_colmajor(tc, host)
-        else:
+            done, i = 0, 0
+            while done < full_clocks:
+                c = min(tc, full_clocks - done)
+                gen.generate_colmajor(c, ring[i & 1][:c])
+                done += c
+                i += 1
+
+        dt = timed(one, steps)
+        d2h = n * full_clocks // 8
+        how = (f"mk2_init_from_material(pinned host keys, IVs) + {ncalls} resumable mk2_generate_colmajor calls of {tc} bits "
+               f"into a ring of two pinned {tc * G * 4 >> 20} MiB host buffers")
+        del ring
+    else:
+        host = torch.empty((n, tc // 8), dtype=torch.uint8).pin_memory()
+        full_clocks = tc
+
+        def one():
             gen.bulk_rowmajor(keys, ivs, 80, tc, host)   # one-shot call: upload | init + keystream | download overlap
 
-    for _ in range(max(1, min(args.warmup, 3))):
-        one()
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
-    torch.cuda.synchronize()
-    dt = max_over_ranks(time.perf_counter() - t0)
-    return {
-        "value": world * n * tc * args.steps / dt / 1e12, "unit": "Tb/s",
-        "h2d_bytes_per_step": int(keys.numel() + ivs.numel()), "d2h_bytes_per_step": int(host.numel() * host.element_size()),
-        "ms_per_step": dt / args.steps * 1e3,
-        "workload": f"bounded sample of the same workload: {n} of {n_full} instances x {tc} bits per GPU per call: "
-                    + ("mk2_init_from_material(pinned host keys, IVs) + mk2_generate_colmajor(pinned host out); "
-                       if layout == "colmajor" else
-                       "mk2_bulk_rowmajor(pinned host keys, IVs -> pinned host out), instance blocks pipelined; ")
-                    + "the host link, not the kernel, bounds it",
+        dt = timed(one, steps)
+        d2h = n * tc // 8
+        how = "mk2_bulk_rowmajor(pinned host keys, IVs -> pinned host out), instance blocks pipelined"
+        del host
+    e2e = {
+        "value": world * n * full_clocks / dt / 1e12, "unit": "Tb/s",
+        "h2d_bytes_per_step": int(keys.numel() + ivs.numel()), "d2h_bytes_per_step": int(d2h),
+        "ms_per_step": dt * 1e3, "steps": steps, "d2h_gb_s": d2h / dt / 1e9,
+        "workload": (f"{n} of {n_full} instances x {full_clocks} of {clocks} bits per GPU per step: " if (n, full_clocks) != (n_full, clocks)
+                     else f"the whole workload, {n} instances x {clocks} bits per GPU per step: ")
+                    + how + "; the host link, not the kernel, bounds it",
     }
+
+    # ---- pageable numpy in / numpy out (bounded sample: one call of tc bits per step)
+    res = {"unit": "Tb/s", "h2d_bytes_per_step": int(keys_np.nbytes + ivs_np.nbytes), "d2h_bytes_per_step": int(n * tc // 8),
+           "steps": steps}
+    if layout == "colmajor":
+        pinned_one = torch.empty((tc, G), dtype=torch.int32).pin_memory()
+        dt_pin = timed(lambda: (gen.init_material(keys, ivs, 80), gen.generate_colmajor(tc, pinned_one)), steps)
+        del pinned_one
+        page = np.empty((tc, G), np.uint32)
+        dt_page = timed(lambda: (gen.init_material(keys_np, ivs_np, 80), gen.generate_colmajor(tc, page)), steps)
+        del page
+        dt_fresh = timed(lambda: pkg.bulk_colmajor(keys_np, ivs_np, 80, tc, device=env.local), steps, warm=2)
+        calls = ("caller-supplied pageable array: mk2_init_from_material + mk2_generate_colmajor",
+                 "pkg.bulk_colmajor(keys, ivs, 80, T) returning a fresh array")
+    else:
+        pinned_one = torch.empty((n, tc // 8), dtype=torch.uint8).pin_memory()
+        dt_pin = timed(lambda: gen.bulk_rowmajor(keys, ivs, 80, tc, pinned_one), steps)
+        del pinned_one
+        page = np.empty((n, tc // 8), np.uint8)
+        dt_page = timed(lambda: gen.bulk_rowmajor(keys_np, ivs_np, 80, tc, page), steps)
+        del page
+        dt_fresh = timed(lambda: pkg.bulk_rowmajor(keys_np, ivs_np, 80, tc, device=env.local), steps, warm=2)
+        calls = ("caller-supplied pageable array: mk2_bulk_rowmajor", "pkg.bulk_rowmajor(keys, ivs, 80, T) returning a fresh array")
+    bits = world * n * tc
+    res.update({
+        "value": bits / dt_page / 1e12, "ms_per_step": dt_page * 1e3, "d2h_gb_s": n * tc / 8 / dt_page / 1e9,
+        "fresh_result_array": {"value": bits / dt_fresh / 1e12, "ms_per_step": dt_fresh * 1e3, "call": calls[1],
+                               "note": "the package's result arrays are page-locked blocks from a cached pool (hostmem.py)"},
+        "pinned_same_sample": {"value": bits / dt_pin / 1e12, "ms_per_step": dt_pin * 1e3},
+        "pageable_over_pinned": dt_pin / dt_page, "fresh_over_pinned": dt_pin / dt_fresh,
+        "workload": f"{n} of {n_full} instances x {tc} bits per GPU per call, pageable numpy key/IV arrays in; value = "
+                    + calls[0] + " (pinned bounce tiles + copy workers inside the library)",
+    })
+    gen.set_async(True)
+    return e2e, res
+
+
+def small_call_latency(env: Env) -> dict:
+    """The reference's batching pattern (cli.py:219-231): one mickey_sliced_words call per 64 lanes.  Wall time of
+    a 64-lane x 4096-clock call with an idle context of the thread reused (the default) and with a new context per
+    call (round 1 behaviour), against the device time of its kernels."""
+    from paper_1909_04750_b200 import hostmem
+
+    pkg = env.pkg
+    mats = [pkg.MickeyKeyIv(KEY, bytes.fromhex("21436587"))] * 64
+
+    def best(fn, reps):
+        v = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            v.append(time.perf_counter() - t0)
+        return min(v) * 1e6, statistics.median(v) * 1e6
+
+    pkg.mickey_sliced_words(mats, 4096, device=env.local)
+    pooled = best(lambda: pkg.mickey_sliced_words(mats, 4096, device=env.local), 30)
+
+    def fresh():
+        hostmem.drop_idle_contexts()
+        pkg.mickey_sliced_words(mats, 4096, device=env.local)
+    unpooled = best(fresh, 8)
+    keys, ivs, nbits, _ = pkg.mickey.pack_materials(mats, 64)
+    pack_us = best(lambda: pkg.mickey.pack_materials(mats, 64), 10)[0]
+    with pkg.MickeyGenerator(env.local) as g:
+        g.init_material(keys, ivs, 32).generate_colmajor(4096)
+        kern, wall = [], []
+        for _ in range(20):
+            t0 = time.perf_counter()
+            g.init_material(keys, ivs, 32)
+            k = g.last_kernel_ms
+            g.generate_colmajor(4096)
+            k += g.last_kernel_ms
+            wall.append(time.perf_counter() - t0)
+            kern.append(k)
+    return {"call": "mickey_sliced_words(64 lanes, 4096 clocks) -> uint64[4096] on the host",
+            "idle_context_reused_us": {"best": pooled[0], "median": pooled[1]},
+            "new_context_per_call_us": {"best": unpooled[0], "median": unpooled[1]},
+            "python_validation_and_packing_us": pack_us,
+            "c_abi_init_plus_generate_us": {"wall_best": min(wall) * 1e6, "device_kernels_best": min(kern) * 1e3},
+            "overhead_over_kernel_time_us": pooled[0] - min(kern) * 1e3,
+            "overhead_over_kernel_time_excluding_python_packing_us": pooled[0] - min(kern) * 1e3 - pack_us}
 
 
 def main():

@@ -32,6 +32,11 @@ thread_local std::string g_create_error;  // text of this thread's last failed m
 // 16x larger (profiles/r01b_probe_e2e_stage.txt).
 constexpr size_t STAGE_BYTES = size_t(32) << 20;
 constexpr size_t ROW_TILE_FACTOR = 16;
+// Pageable host outputs: a staging tile crosses the link in sub-chunks of BOUNCE_BYTES through a ring of
+// BOUNCE_SLOTS pinned slots (96 MiB of page-locked memory per context, allocated on first use).
+constexpr size_t BOUNCE_BYTES = size_t(32) << 20;
+constexpr int BOUNCE_SLOTS = 3;
+constexpr uint64_t BOUNCE_MIN_BYTES = uint64_t(8) << 20;
 
 // Restores the caller's current device when an entry point returns: a process that drives torch on cuda:0 and
 // an mk2 context on device 1 keeps its own current device.
@@ -78,7 +83,6 @@ public:
         cv_.notify_all();
         for (auto &t : workers_) t.join();
     }
-    int threads() const { return (int)workers_.size() + 1; }
     // dst[r * dpitch .. + width) = src[r * spitch .. + width) for r < rows; returns when done
     void copy2d(uint8_t *dst, size_t dpitch, const uint8_t *src, size_t spitch, size_t width, size_t rows)
     {
@@ -193,8 +197,8 @@ struct mk2_ctx {
     unsigned max_grid = 0;               // debug knob: cap on persistent CTAs (0 = one per SM slot)
     void *d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
-    void *h_bounce[2] = {nullptr, nullptr};  // pinned bounce buffers for PAGEABLE host outputs (one per staging tile)
-    size_t bounce_bytes = 0;
+    void *h_bounce = nullptr;                // pinned bounce ring for PAGEABLE host outputs: BOUNCE_SLOTS x BOUNCE_BYTES
+    cudaEvent_t sub_done[4] = {nullptr, nullptr, nullptr, nullptr};  // D2H of a bounce slot complete
     HostCopyPool *copy_pool = nullptr;       // worker threads that move bounce tiles into pageable memory (lazy)
     int host_threads = 0;                    // 0 = automatic
     bool ready = false, async = false, timing_open = false;
@@ -328,27 +332,24 @@ int ensure_stage(mk2_ctx *ctx, size_t bytes)
     return MK2_OK;
 }
 
-// Pinned bounce buffers + copy workers for pageable host outputs (see HostCopyPool).
-int ensure_bounce(mk2_ctx *ctx, size_t bytes)
+// Pinned bounce ring + copy workers for pageable host outputs (see HostCopyPool, HostTiles).
+int ensure_bounce(mk2_ctx *ctx)
 {
     if (!ctx->copy_pool) {
         int n = ctx->host_threads;
         if (n <= 0) {
+            // measured on the 16-core B200 host (profiles/r02_probe_host_buffers.txt): 8 threads move 46 GB/s into
+            // touched pageable memory, 16 threads 53 GB/s (pinned: 56.6 GB/s), so every core up to 16 is used
             const unsigned hw = std::thread::hardware_concurrency();
-            n = (int)std::min<unsigned>(8u, std::max<unsigned>(2u, hw / 2));
+            n = (int)std::min<unsigned>(16u, std::max<unsigned>(2u, hw));
         }
         ctx->copy_pool = new (std::nothrow) HostCopyPool(n - 1);  // the calling thread is the n-th worker
         if (!ctx->copy_pool) return fail(ctx, MK2_E_NOMEM, "out of host memory");
     }
-    if (bytes <= ctx->bounce_bytes) return MK2_OK;
-    CK(cudaStreamSynchronize(ctx->copy));
-    for (int b = 0; b < 2; ++b) {
-        if (ctx->h_bounce[b]) cudaFreeHost(ctx->h_bounce[b]);
-        ctx->h_bounce[b] = nullptr;
-    }
-    ctx->bounce_bytes = 0;
-    for (int b = 0; b < 2; ++b) CK(cudaHostAlloc(&ctx->h_bounce[b], bytes, cudaHostAllocDefault));
-    ctx->bounce_bytes = bytes;
+    if (ctx->h_bounce) return MK2_OK;
+    for (int i = 0; i < BOUNCE_SLOTS; ++i)
+        if (!ctx->sub_done[i]) CK(cudaEventCreateWithFlags(&ctx->sub_done[i], cudaEventDisableTiming));
+    CK(cudaHostAlloc(&ctx->h_bounce, BOUNCE_BYTES * BOUNCE_SLOTS, cudaHostAllocDefault));
     return MK2_OK;
 }
 
@@ -578,75 +579,106 @@ int drain_copies(mk2_ctx *ctx)
 
 // D2H side of a host-output call.  Tile i is generated into device staging buffer b = i & 1 (caller:
 // acquire_stage + launch), then copy_out() moves it to the caller's array:
-//   pinned destination   -> one async (2-D) copy on the copy stream, straight into the array;
-//   pageable destination -> async copy into pinned bounce buffer b at link speed; the calling thread and the
-//                           copy workers move bounce tile i-1 into the array while tile i crosses the link
-//                           and tile i+1 is generated.
+//   pinned destination   -> one async (2-D) copy on the copy stream, straight into the array, overlapping the
+//                           generation of the next tile (two staging buffers);
+//   pageable destination -> copy_out(i) first records kernel i's completion event and then PUMPS tile i-1 (whose
+//                           kernel has long finished) while kernel i runs: the tile crosses the link in
+//                           sub-chunks of BOUNCE_BYTES through a ring of pinned slots, up to BOUNCE_SLOTS - 1
+//                           sub-copies queued ahead while the calling thread and the copy workers move the
+//                           landed slot into the caller's array.  The link stays busy; the exposed tail of a
+//                           call is one sub-chunk, whatever the tile size.
 // finish() waits for everything (the API returns with the array complete).
 class HostTiles {
 public:
-    HostTiles(mk2_ctx *c, bool pageable) : ctx(c), bounce(pageable) {}
-    bool pageable() const { return bounce; }
-    int prepare(size_t tile_bytes) { return bounce ? ensure_bounce(ctx, tile_bytes) : MK2_OK; }
+    // Small pageable outputs are not worth the ring (and its one-time 96 MiB page-locking): the driver's own
+    // staged copy handles them.
+    HostTiles(mk2_ctx *c, Mem dst, uint64_t total_bytes) : ctx(c), bounce(dst == Mem::Pageable && total_bytes >= BOUNCE_MIN_BYTES) {}
+    int prepare() { return bounce ? ensure_bounce(ctx) : MK2_OK; }
     int next() { return (int)(count++ & 1); }
     // rows x width bytes from staging buffer b (pitch spitch) to dst (pitch dpitch)
     int copy_out(int b, uint8_t *dst, size_t dpitch, size_t spitch, size_t width, size_t rows)
     {
         CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
-        CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
-        if (!bounce) {
-            if (dpitch == width && spitch == width)
-                CK(cudaMemcpyAsync(dst, ctx->d_stage[b], width * rows, cudaMemcpyDeviceToHost, ctx->copy));
-            else
-                CK(cudaMemcpy2DAsync(dst, dpitch, ctx->d_stage[b], spitch, width, rows, cudaMemcpyDeviceToHost, ctx->copy));
-        } else {
-            // bounce buffer b still holds tile i-2 until the workers have moved it out: flush it first
-            int rc = flush(b);
+        if (bounce) {
+            int rc = pump();  // the previous tile, while this one is being generated
             if (rc) return rc;
-            if (spitch == width)
-                CK(cudaMemcpyAsync(ctx->h_bounce[b], ctx->d_stage[b], width * rows, cudaMemcpyDeviceToHost, ctx->copy));
-            else
-                CK(cudaMemcpy2DAsync(ctx->h_bounce[b], width, ctx->d_stage[b], spitch, width, rows, cudaMemcpyDeviceToHost,
-                                     ctx->copy));
-            pend[b] = {dst, dpitch, width, rows, true};
+            pend = {b, dst, dpitch, spitch, width, rows, true};
+            return MK2_OK;
         }
+        CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
+        if (dpitch == width && spitch == width)
+            CK(cudaMemcpyAsync(dst, ctx->d_stage[b], width * rows, cudaMemcpyDeviceToHost, ctx->copy));
+        else
+            CK(cudaMemcpy2DAsync(dst, dpitch, ctx->d_stage[b], spitch, width, rows, cudaMemcpyDeviceToHost, ctx->copy));
         CK(cudaEventRecord(ctx->copy_done[b], ctx->copy));
         ctx->copy_pending[b] = true;
-        if (bounce) {  // move the PREVIOUS tile out while this one is in flight
-            int rc = flush(b ^ 1);
-            if (rc) return rc;
-        }
         return MK2_OK;
     }
     int finish()
     {
         if (bounce) {
-            int rc;
-            const int last = (int)((count + 1) & 1);  // older tile first
-            if ((rc = flush(last ^ 1)) || (rc = flush(last))) return rc;
+            int rc = pump();
+            if (rc) return rc;
         }
         return drain_copies(ctx);
     }
 
 private:
     struct Pending {
+        int b = 0;
         uint8_t *dst = nullptr;
-        size_t dpitch = 0, width = 0, rows = 0;
+        size_t dpitch = 0, spitch = 0, width = 0, rows = 0;
         bool live = false;
     };
-    int flush(int b)
+    // Move the pending tile out: staging buffer -> pinned slots (copy stream) -> caller's array (copy workers).
+    // Returns with the staging buffer free again, so the caller needs no stream-side wait before reusing it.
+    int pump()
     {
-        if (!pend[b].live) return MK2_OK;
-        CK(cudaEventSynchronize(ctx->copy_done[b]));
-        ctx->copy_pool->copy2d(pend[b].dst, pend[b].dpitch, static_cast<const uint8_t *>(ctx->h_bounce[b]), pend[b].width,
-                               pend[b].width, pend[b].rows);
-        pend[b].live = false;
+        if (!pend.live) return MK2_OK;
+        pend.live = false;
+        const Pending t = pend;
+        CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[t.b], 0));
+        // sub-chunks: whole rows (narrow rows) or pieces of one row (rows wider than a slot)
+        const size_t rows_per_sub = std::max<size_t>(1, BOUNCE_BYTES / t.width);
+        const size_t cols_per_sub = t.width <= BOUNCE_BYTES ? t.width : BOUNCE_BYTES;
+        const size_t col_subs = (t.width + cols_per_sub - 1) / cols_per_sub;
+        const size_t row_subs = (t.rows + rows_per_sub - 1) / rows_per_sub;
+        const size_t nsub = row_subs * col_subs;
+        const uint8_t *src = static_cast<const uint8_t *>(ctx->d_stage[t.b]);
+        uint8_t *ring = static_cast<uint8_t *>(ctx->h_bounce);
+        auto geom = [&](size_t i, size_t &r0, size_t &nr, size_t &c0, size_t &nc) {
+            r0 = (i / col_subs) * rows_per_sub;
+            nr = std::min(rows_per_sub, t.rows - r0);
+            c0 = (i % col_subs) * cols_per_sub;
+            nc = std::min(cols_per_sub, t.width - c0);
+        };
+        size_t issued = 0, done = 0;
+        while (done < nsub) {
+            while (issued < nsub && issued - done < (size_t)BOUNCE_SLOTS) {
+                size_t r0, nr, c0, nc;
+                geom(issued, r0, nr, c0, nc);
+                const int slot = (int)(issued % BOUNCE_SLOTS);
+                uint8_t *h = ring + (size_t)slot * BOUNCE_BYTES;
+                if (t.spitch == nc)
+                    CK(cudaMemcpyAsync(h, src + r0 * t.spitch, nc * nr, cudaMemcpyDeviceToHost, ctx->copy));
+                else
+                    CK(cudaMemcpy2DAsync(h, nc, src + r0 * t.spitch + c0, t.spitch, nc, nr, cudaMemcpyDeviceToHost, ctx->copy));
+                CK(cudaEventRecord(ctx->sub_done[slot], ctx->copy));
+                ++issued;
+            }
+            size_t r0, nr, c0, nc;
+            geom(done, r0, nr, c0, nc);
+            const int slot = (int)(done % BOUNCE_SLOTS);
+            CK(cudaEventSynchronize(ctx->sub_done[slot]));
+            ctx->copy_pool->copy2d(t.dst + r0 * t.dpitch + c0, t.dpitch, ring + (size_t)slot * BOUNCE_BYTES, nc, nc, nr);
+            ++done;
+        }
         return MK2_OK;
     }
     mk2_ctx *ctx;
     bool bounce;
     uint64_t count = 0;
-    Pending pend[2];
+    Pending pend;
 };
 
 int check_ready(mk2_ctx *ctx)
@@ -800,10 +832,12 @@ int mk2_destroy(mk2_ctx *ctx)
         if (ctx->h2d_done[b]) cudaEventDestroy(ctx->h2d_done[b]);
         if (ctx->mat_used[b]) cudaEventDestroy(ctx->mat_used[b]);
         if (ctx->d_stage[b]) cudaFree(ctx->d_stage[b]);
-        if (ctx->h_bounce[b]) cudaFreeHost(ctx->h_bounce[b]);
         if (ctx->gen_done[b]) cudaEventDestroy(ctx->gen_done[b]);
         if (ctx->copy_done[b]) cudaEventDestroy(ctx->copy_done[b]);
     }
+    if (ctx->h_bounce) cudaFreeHost(ctx->h_bounce);
+    for (auto &e : ctx->sub_done)
+        if (e) cudaEventDestroy(e);
     if (ctx->d_state) cudaFree(ctx->d_state);
     if (ctx->d_acc) cudaFree(ctx->d_acc);
     if (ctx->d_sum) cudaFree(ctx->d_sum);
@@ -1299,8 +1333,8 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
         const size_t row_bytes = ctx->G * sizeof(uint32_t);
         const size_t want = std::max<size_t>(std::min<size_t>(ctx->stage_target, T * row_bytes), row_bytes);
         if ((rc = ensure_stage(ctx, want))) return rc;
-        HostTiles tiles(ctx, mem == Mem::Pageable);
-        if ((rc = tiles.prepare(ctx->stage_bytes))) return rc;
+        HostTiles tiles(ctx, mem, T * row_bytes);
+        if ((rc = tiles.prepare())) return rc;
         const uint64_t chunk = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
         for (uint64_t t0 = 0; t0 < T; t0 += chunk) {
             const uint64_t tc = std::min(chunk, T - t0);
@@ -1328,18 +1362,16 @@ static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pit
     // tile = [block_chains x 1024 rows] x [tc_max clocks] of about ROW_TILE_FACTOR x stage_target bytes, rows at
     // least 512 B wide when T allows (narrower 2-D copies collapse: 192 B rows 37 GB/s, 64 B rows 16 GB/s), and
     // between one and two chains per worker warp of a full launch
-    // (pageable destinations: a quarter of that, because the last tile's move out of the bounce buffer is exposed
-    // at the end of the call; the link, not the kernel, is the bottleneck, so smaller launches cost nothing)
-    const uint64_t tile_bytes = (tiles.pageable() ? ROW_TILE_FACTOR / 4 : ROW_TILE_FACTOR) * ctx->stage_target;
+    const uint64_t tile_bytes = ROW_TILE_FACTOR * ctx->stage_target;
     const uint64_t min_clocks = std::min<uint64_t>((T + 255) / 256 * 256, 4096);
-    const uint64_t workers = (tiles.pageable() ? 2ull : 8ull) * (uint64_t)ctx->sm_count;
+    const uint64_t workers = 8ull * (uint64_t)ctx->sm_count;
     const uint64_t want_chains = std::min<uint64_t>(2 * workers, std::max<uint64_t>(workers, tile_bytes / (min_clocks / 8) / 1024));
     const uint64_t block_chains = std::min<uint64_t>(chains, want_chains);
     const uint64_t block_rows = block_chains * 1024;
     uint64_t tc_max = std::max<uint64_t>(min_clocks, tile_bytes / block_rows / 32 * 256);
     tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
     if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
-    if ((rc = tiles.prepare(ctx->stage_bytes))) return rc;
+    if ((rc = tiles.prepare())) return rc;
     for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {
         const uint64_t nch = std::min(block_chains, chains - c0);
         const uint64_t row0 = c0 * 1024;
@@ -1374,7 +1406,7 @@ static int generate_rowmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
     if (mem == Mem::Device) {
         if ((rc = launch_row(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, 0, chains))) return rc;
     } else {
-        HostTiles tiles(ctx, mem == Mem::Pageable);
+        HostTiles tiles(ctx, mem, ctx->N * (T / 8));
         if ((rc = rowmajor_to_host(ctx, T, static_cast<uint8_t *>(out), pitch_bytes, tiles))) return rc;
         if ((rc = tiles.finish())) return rc;
     }
@@ -1454,7 +1486,7 @@ static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *
     CK(cudaMemsetAsync(ctx->d_sum, 0, sizeof(unsigned long long), ctx->stream));
     CK(cudaEventRecord(ctx->mat_used[0], ctx->stream));  // everything queued before this call is ahead of the uploads
     CK(cudaStreamWaitEvent(ctx->h2d, ctx->mat_used[0], 0));
-    HostTiles tiles(ctx, out_mem == Mem::Pageable);
+    HostTiles tiles(ctx, out_mem, N * (T / 8));
     ctx->row_lsb = false;
     int launches = 0;
     uint64_t nblk = 0;

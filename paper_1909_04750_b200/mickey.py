@@ -108,7 +108,32 @@ def pack_materials(materials: Sequence, width: int):
     keys = np.zeros((width, KEY_BYTES), np.uint8)
     ivs = np.zeros((width, 10), np.uint8)
     nbits = np.zeros(width, np.uint8)
+    n = len(materials)
+    if all(type(m) is MickeyKeyIv and type(m.iv) is bytes for m in materials):
+        # the common case, without a Python-level loop over bits: records validated at construction
+        # (__post_init__), byte strings already in the MSB-first wire order
+        keys[:n] = np.frombuffer(b"".join(m.key for m in materials), np.uint8).reshape(n, KEY_BYTES)
+        lens = {len(m.iv) for m in materials}
+        if len(lens) == 1:
+            (ln,) = lens
+            if ln:
+                ivs[:n, :ln] = np.frombuffer(b"".join(m.iv for m in materials), np.uint8).reshape(n, ln)
+            nbits[:] = 8 * ln      # uniform: unused lanes load zero bits for the same clock count
+            return keys, ivs, nbits, True
+        for lane, m in enumerate(materials):
+            if m.iv:
+                ivs[lane, : len(m.iv)] = np.frombuffer(m.iv, np.uint8)
+            nbits[lane] = 8 * len(m.iv)
+        nbits[n:] = MK2_IV_UNUSED
+        return keys, ivs, nbits, False
     for lane, m in enumerate(materials):
+        if type(m) is MickeyKeyIv and type(m.iv) is bytes:
+            # validated at construction (__post_init__); byte strings are already in the MSB-first wire order
+            keys[lane] = np.frombuffer(m.key, np.uint8)
+            if m.iv:
+                ivs[lane, : len(m.iv)] = np.frombuffer(m.iv, np.uint8)
+            nbits[lane] = 8 * len(m.iv)
+            continue
         try:
             iv = m.iv_bits()
             key = m.key_bits()
