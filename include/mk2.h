@@ -20,12 +20,14 @@
  *   pinned host      (cudaHostAlloc / cudaHostRegister / mk2_host_alloc /
  *                    torch pin_memory) outputs receive asynchronous D2H copies
  *                    of the device staging tiles directly, at link speed;
- *   pageable host    (malloc, a fresh numpy array) outputs go through two
- *                    pinned bounce buffers owned by the context, and a small
- *                    pool of host threads (mk2_set_host_threads) moves each
- *                    bounce tile into the caller's array while the next tile
- *                    crosses the link; pageable inputs (key/IV bytes, 20 B per
- *                    instance) are plain cudaMemcpyAsync calls.
+ *   pageable host    (malloc, a fresh numpy array) outputs of 8 MiB or more are
+ *                    moved by the context's copy lanes (mk2_set_host_threads):
+ *                    host threads with their own stream and 4 MiB page-locked
+ *                    slot that each copy sub-chunks of the device staging tile
+ *                    to the slot and memcpy them into the caller's array, so
+ *                    several D2H copies are in flight while others are being
+ *                    moved; smaller outputs and pageable inputs (key/IV bytes,
+ *                    20 B per instance) are plain cudaMemcpyAsync calls.
  * Every output call returns with the caller's array complete.
  *
  * Current device: every entry point runs on its context's device and restores
@@ -230,8 +232,8 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
  * in flight: one being generated, one being copied out).  0 = default (32 MiB;
  * row-major tiles, which are 2-D copies, are 16x this). */
 int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes);
-/* Host threads (the calling thread included) that move bounce tiles into
- * PAGEABLE output arrays; 0 = automatic (half the hardware threads, 2..8). */
+/* Number of copy lanes (host threads) that move staging tiles into PAGEABLE
+ * output arrays; 0 = automatic (one per hardware thread, 2..16). */
 int mk2_set_host_threads(mk2_ctx *ctx, int threads);
 /* Pinned (page-locked, portable) host memory for output arrays that should take
  * the direct D2H path: what the Python front end's fresh result arrays are made

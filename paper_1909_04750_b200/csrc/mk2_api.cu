@@ -9,6 +9,7 @@
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -32,10 +33,7 @@ thread_local std::string g_create_error;  // text of this thread's last failed m
 // 16x larger (profiles/r01b_probe_e2e_stage.txt).
 constexpr size_t STAGE_BYTES = size_t(32) << 20;
 constexpr size_t ROW_TILE_FACTOR = 16;
-// Pageable host outputs: a staging tile crosses the link in sub-chunks of BOUNCE_BYTES through a ring of
-// BOUNCE_SLOTS pinned slots (96 MiB of page-locked memory per context, allocated on first use).
-constexpr size_t BOUNCE_BYTES = size_t(32) << 20;
-constexpr int BOUNCE_SLOTS = 3;
+// Pageable host outputs below this size are left to the driver's own staged copy (no lanes, no page-locking).
 constexpr uint64_t BOUNCE_MIN_BYTES = uint64_t(8) << 20;
 
 // Restores the caller's current device when an entry point returns: a process that drives torch on cuda:0 and
@@ -61,110 +59,142 @@ struct DeviceGuard {
 
 // ---------------------------------------------------------------------------
 // Host side of PAGEABLE output buffers.  A D2H copy into pageable memory is staged by the driver
-// through its own small pinned buffers on the calling thread (measured on this box: ~10 GB/s against
-// 55 GB/s into pinned memory).  Here the device staging tile is copied into one of two pinned bounce
-// buffers at link speed and a few worker threads move the previous bounce tile into the caller's
-// array meanwhile (a fresh numpy array also takes its first-touch page faults there, in parallel).
-// One job at a time: a 2-D block copy cut into row slices that the workers (and the calling thread)
-// claim from an atomic counter.
+// through its own small pinned buffers on the calling thread (measured on this box: 10-13 GB/s against
+// 56 GB/s into pinned memory).  Here a few independent COPY LANES do it in parallel: a lane is a host
+// thread with its own CUDA stream, event and page-locked slot.  A device staging tile is cut into
+// sub-chunks of LANE_BYTES; every lane repeatedly claims the next sub-chunk, copies it device -> slot on
+// its stream, waits for it and memcpy's the slot into the caller's array (a fresh numpy array takes its
+// first-touch page faults there, spread over the lanes).  While one lane is in memcpy the others have
+// their D2H copies in flight, so the link stays busy; tiles are queued, so the lanes run on into the
+// next tile while the calling thread is launching kernels.
 // ---------------------------------------------------------------------------
-class HostCopyPool {
+constexpr size_t LANE_BYTES = size_t(4) << 20;
+
+class HostCopyLanes {
 public:
-    explicit HostCopyPool(int nthreads)
+    struct Tile {
+        const uint8_t *src = nullptr;  // device staging buffer
+        uint8_t *dst = nullptr;        // caller's (pageable) array
+        size_t spitch = 0, dpitch = 0, width = 0, rows = 0;
+        cudaEvent_t ready = nullptr;   // recorded after the kernel that fills src
+        size_t rows_per_sub = 1, cols_per_sub = 1, col_subs = 1, nsub = 0;
+        std::atomic<size_t> next{0};
+        std::atomic<size_t> remaining{0};
+        std::atomic<int> error{0};     // first cudaError_t seen by a lane
+        unsigned long long id = 0;     // never reused (a freed tile's address can be)
+    };
+    using TilePtr = std::shared_ptr<Tile>;
+
+    HostCopyLanes(int device, int nlanes) : device_(device)
     {
-        for (int i = 0; i < nthreads; ++i) workers_.emplace_back([this] { run(); });
+        for (int i = 0; i < nlanes; ++i) lanes_.emplace_back([this] { run(); });
     }
-    ~HostCopyPool()
+    ~HostCopyLanes()
     {
         {
             std::lock_guard<std::mutex> lk(m_);
             stop_ = true;
         }
         cv_.notify_all();
-        for (auto &t : workers_) t.join();
+        for (auto &t : lanes_) t.join();
     }
-    // dst[r * dpitch .. + width) = src[r * spitch .. + width) for r < rows; returns when done
-    void copy2d(uint8_t *dst, size_t dpitch, const uint8_t *src, size_t spitch, size_t width, size_t rows)
+    // rows x width bytes at src (pitch spitch, device) -> dst (pitch dpitch, host), once `ready` has happened
+    TilePtr post(const void *src, size_t spitch, void *dst, size_t dpitch, size_t width, size_t rows, cudaEvent_t ready)
     {
-        if (rows == 0 || width == 0) return;
-        if (dpitch == width && spitch == width) {  // contiguous: one long row
-            width *= rows;
-            rows = 1;
-            dpitch = spitch = width;
-        }
-        auto j = std::make_shared<Job>();
-        j->dst = dst; j->src = src; j->dpitch = dpitch; j->spitch = spitch; j->width = width; j->rows = rows;
-        // slices of about 1 MiB: row ranges or, for one long row, byte ranges
-        if (rows == 1) {
-            j->slice = size_t(1) << 20;
-            j->nslices = (width + j->slice - 1) / j->slice;
-        } else {
-            j->slice = std::max<size_t>(1, (size_t(1) << 20) / width);
-            j->nslices = (rows + j->slice - 1) / j->slice;
-        }
-        j->pending = j->nslices;
+        auto t = std::make_shared<Tile>();
+        t->src = static_cast<const uint8_t *>(src);
+        t->dst = static_cast<uint8_t *>(dst);
+        t->spitch = spitch; t->dpitch = dpitch; t->width = width; t->rows = rows; t->ready = ready;
+        // sub-chunks: whole rows (narrow rows) or pieces of one row (rows wider than a slot)
+        t->rows_per_sub = std::max<size_t>(1, LANE_BYTES / width);
+        t->cols_per_sub = std::min(width, LANE_BYTES);
+        t->col_subs = (width + t->cols_per_sub - 1) / t->cols_per_sub;
+        t->nsub = ((rows + t->rows_per_sub - 1) / t->rows_per_sub) * t->col_subs;
+        t->remaining.store(t->nsub);
+        if (t->nsub == 0) return t;
         {
             std::lock_guard<std::mutex> lk(m_);
-            job_ = j;
-            ++generation_;
+            t->id = ++last_id_;
+            queue_.push_back(t);
         }
         cv_.notify_all();
-        work(*j);
+        return t;
+    }
+    // blocks until every sub-chunk of the tile is in the caller's array; returns the first CUDA error (0 = none)
+    int wait(const TilePtr &t)
+    {
+        if (!t) return 0;
         std::unique_lock<std::mutex> lk(m_);
-        done_.wait(lk, [&] { return j->pending == 0; });
-        job_.reset();
+        done_.wait(lk, [&] { return t->remaining.load() == 0; });
+        return t->error.load();
     }
 
 private:
-    // Every job owns its slice counter, so a worker that wakes up late only finds an exhausted job.
-    struct Job {
-        uint8_t *dst = nullptr;
-        const uint8_t *src = nullptr;
-        size_t dpitch = 0, spitch = 0, width = 0, rows = 0, slice = 1, nslices = 0;
-        std::atomic<size_t> next{0};
-        size_t pending = 0;  // guarded by m_
-    };
-    void work(Job &j)
-    {
-        size_t finished = 0;
-        for (;;) {
-            const size_t i = j.next.fetch_add(1, std::memory_order_relaxed);
-            if (i >= j.nslices) break;
-            if (j.rows == 1) {
-                const size_t o = i * j.slice, n = std::min(j.slice, j.width - o);
-                std::memcpy(j.dst + o, j.src + o, n);
-            } else {
-                const size_t r0 = i * j.slice, r1 = std::min(j.rows, r0 + j.slice);
-                for (size_t r = r0; r < r1; ++r) std::memcpy(j.dst + r * j.dpitch, j.src + r * j.spitch, j.width);
-            }
-            ++finished;
-        }
-        if (finished) {
-            std::lock_guard<std::mutex> lk(m_);
-            j.pending -= finished;
-            if (j.pending == 0) done_.notify_all();
-        }
-    }
     void run()
     {
-        unsigned long long seen = 0;
+        cudaStream_t stream = nullptr;
+        cudaEvent_t ev = nullptr;
+        void *slot = nullptr;
+        bool ok = cudaSetDevice(device_) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaHostAlloc(&slot, LANE_BYTES, cudaHostAllocDefault) == cudaSuccess;
+        unsigned long long synced = 0;  // id of the tile whose `ready` event this lane's stream already waits on
         for (;;) {
-            std::shared_ptr<Job> j;
+            TilePtr t;
             {
                 std::unique_lock<std::mutex> lk(m_);
-                cv_.wait(lk, [&] { return stop_ || generation_ != seen; });
-                if (stop_) return;
-                seen = generation_;
-                j = job_;
+                for (;;) {
+                    while (!queue_.empty() && queue_.front()->next.load() >= queue_.front()->nsub) queue_.pop_front();
+                    if (stop_ || !queue_.empty()) break;
+                    cv_.wait(lk);
+                }
+                if (stop_) break;
+                t = queue_.front();
             }
-            if (j) work(*j);
+            const size_t i = t->next.fetch_add(1);
+            if (i >= t->nsub) continue;
+            cudaError_t e = ok ? cudaSuccess : cudaErrorInitializationError;
+            const size_t r0 = (i / t->col_subs) * t->rows_per_sub, nr = std::min(t->rows_per_sub, t->rows - r0);
+            const size_t c0 = (i % t->col_subs) * t->cols_per_sub, nc = std::min(t->cols_per_sub, t->width - c0);
+            if (e == cudaSuccess && synced != t->id) {
+                e = cudaStreamWaitEvent(stream, t->ready, 0);
+                synced = t->id;
+            }
+            if (e == cudaSuccess) {
+                if (t->spitch == nc)
+                    e = cudaMemcpyAsync(slot, t->src + r0 * t->spitch, nc * nr, cudaMemcpyDeviceToHost, stream);
+                else
+                    e = cudaMemcpy2DAsync(slot, nc, t->src + r0 * t->spitch + c0, t->spitch, nc, nr, cudaMemcpyDeviceToHost, stream);
+            }
+            if (e == cudaSuccess) e = cudaEventRecord(ev, stream);
+            if (e == cudaSuccess) e = cudaEventSynchronize(ev);
+            if (e == cudaSuccess) {
+                uint8_t *d = t->dst + r0 * t->dpitch + c0;
+                const uint8_t *h = static_cast<const uint8_t *>(slot);
+                if (t->dpitch == nc) std::memcpy(d, h, nc * nr);
+                else
+                    for (size_t r = 0; r < nr; ++r) std::memcpy(d + r * t->dpitch, h + r * nc, nc);
+            } else {
+                int zero = 0;
+                t->error.compare_exchange_strong(zero, (int)e);
+                cudaGetLastError();
+            }
+            if (t->remaining.fetch_sub(1) == 1) {
+                std::lock_guard<std::mutex> lk(m_);
+                done_.notify_all();
+            }
         }
+        if (slot) cudaFreeHost(slot);
+        if (ev) cudaEventDestroy(ev);
+        if (stream) cudaStreamDestroy(stream);
     }
-    std::vector<std::thread> workers_;
+    int device_;
+    std::vector<std::thread> lanes_;
     std::mutex m_;
     std::condition_variable cv_, done_;
-    std::shared_ptr<Job> job_;
-    unsigned long long generation_ = 0;
+    std::deque<TilePtr> queue_;
+    unsigned long long last_id_ = 0;
     bool stop_ = false;
 };
 }  // namespace
@@ -197,10 +227,8 @@ struct mk2_ctx {
     unsigned max_grid = 0;               // debug knob: cap on persistent CTAs (0 = one per SM slot)
     void *d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
-    void *h_bounce = nullptr;                // pinned bounce ring for PAGEABLE host outputs: BOUNCE_SLOTS x BOUNCE_BYTES
-    cudaEvent_t sub_done[4] = {nullptr, nullptr, nullptr, nullptr};  // D2H of a bounce slot complete
-    HostCopyPool *copy_pool = nullptr;       // worker threads that move bounce tiles into pageable memory (lazy)
-    int host_threads = 0;                    // 0 = automatic
+    HostCopyLanes *lanes = nullptr;          // copy lanes for PAGEABLE host outputs (lazy)
+    int host_threads = 0;                    // number of lanes; 0 = automatic
     bool ready = false, async = false, timing_open = false;
     int cipher = 0;        // 0 = MICKEY 2.0, 1 = Grain v1 (which kernels the state belongs to)
     bool row_lsb = false;  // Grain row-major byte packing of the current call
@@ -332,24 +360,19 @@ int ensure_stage(mk2_ctx *ctx, size_t bytes)
     return MK2_OK;
 }
 
-// Pinned bounce ring + copy workers for pageable host outputs (see HostCopyPool, HostTiles).
-int ensure_bounce(mk2_ctx *ctx)
+// Copy lanes for pageable host outputs (see HostCopyLanes, HostTiles).
+int ensure_lanes(mk2_ctx *ctx)
 {
-    if (!ctx->copy_pool) {
-        int n = ctx->host_threads;
-        if (n <= 0) {
-            // measured on the 16-core B200 host (profiles/r02_probe_host_buffers.txt): 8 threads move 46 GB/s into
-            // touched pageable memory, 16 threads 53 GB/s (pinned: 56.6 GB/s), so every core up to 16 is used
-            const unsigned hw = std::thread::hardware_concurrency();
-            n = (int)std::min<unsigned>(16u, std::max<unsigned>(2u, hw));
-        }
-        ctx->copy_pool = new (std::nothrow) HostCopyPool(n - 1);  // the calling thread is the n-th worker
-        if (!ctx->copy_pool) return fail(ctx, MK2_E_NOMEM, "out of host memory");
+    if (ctx->lanes) return MK2_OK;
+    int n = ctx->host_threads;
+    if (n <= 0) {
+        // every core up to 16 (profiles/r02_probe_host_buffers.txt: the lanes alternate between waiting for their
+        // D2H copy and memcpy, so more lanes than memcpy alone would need keep the link busy)
+        const unsigned hw = std::thread::hardware_concurrency();
+        n = (int)std::min<unsigned>(16u, std::max<unsigned>(2u, hw));
     }
-    if (ctx->h_bounce) return MK2_OK;
-    for (int i = 0; i < BOUNCE_SLOTS; ++i)
-        if (!ctx->sub_done[i]) CK(cudaEventCreateWithFlags(&ctx->sub_done[i], cudaEventDisableTiming));
-    CK(cudaHostAlloc(&ctx->h_bounce, BOUNCE_BYTES * BOUNCE_SLOTS, cudaHostAllocDefault));
+    ctx->lanes = new (std::nothrow) HostCopyLanes(ctx->device, n);
+    if (!ctx->lanes) return fail(ctx, MK2_E_NOMEM, "out of host memory");
     return MK2_OK;
 }
 
@@ -577,32 +600,37 @@ int drain_copies(mk2_ctx *ctx)
     return MK2_OK;
 }
 
-// D2H side of a host-output call.  Tile i is generated into device staging buffer b = i & 1 (caller:
-// acquire_stage + launch), then copy_out() moves it to the caller's array:
-//   pinned destination   -> one async (2-D) copy on the copy stream, straight into the array, overlapping the
-//                           generation of the next tile (two staging buffers);
-//   pageable destination -> copy_out(i) first records kernel i's completion event and then PUMPS tile i-1 (whose
-//                           kernel has long finished) while kernel i runs: the tile crosses the link in
-//                           sub-chunks of BOUNCE_BYTES through a ring of pinned slots, up to BOUNCE_SLOTS - 1
-//                           sub-copies queued ahead while the calling thread and the copy workers move the
-//                           landed slot into the caller's array.  The link stays busy; the exposed tail of a
-//                           call is one sub-chunk, whatever the tile size.
+// D2H side of a host-output call.  Tile i is generated into device staging buffer b = i & 1; the caller does
+//     b = next(); acquire(b); <launch the kernel into d_stage[b]>; copy_out(b, ...)
+//   pinned destination   -> one async (2-D) copy on the copy stream, straight into the array; acquire() makes the
+//                           launch stream wait for the copy that last read the buffer;
+//   pageable destination -> the tile is queued for the copy lanes (HostCopyLanes), which start on it as soon as
+//                           its kernel has finished; acquire() blocks the calling thread until the lanes have
+//                           moved the tile that last used the buffer.
 // finish() waits for everything (the API returns with the array complete).
 class HostTiles {
 public:
-    // Small pageable outputs are not worth the ring (and its one-time 96 MiB page-locking): the driver's own
-    // staged copy handles them.
+    // Small pageable outputs are not worth the lanes: the driver's own staged copy handles them.
     HostTiles(mk2_ctx *c, Mem dst, uint64_t total_bytes) : ctx(c), bounce(dst == Mem::Pageable && total_bytes >= BOUNCE_MIN_BYTES) {}
-    int prepare() { return bounce ? ensure_bounce(ctx) : MK2_OK; }
+    ~HostTiles()
+    {
+        // never leave lanes writing into the caller's array (or reading a staging buffer) after the call returned
+        if (bounce && ctx->lanes)
+            for (auto &t : inflight) ctx->lanes->wait(t);
+    }
+    int prepare() { return bounce ? ensure_lanes(ctx) : MK2_OK; }
     int next() { return (int)(count++ & 1); }
+    int acquire(int b)
+    {
+        if (!bounce) return acquire_stage(ctx, b);
+        return reclaim(b);
+    }
     // rows x width bytes from staging buffer b (pitch spitch) to dst (pitch dpitch)
     int copy_out(int b, uint8_t *dst, size_t dpitch, size_t spitch, size_t width, size_t rows)
     {
         CK(cudaEventRecord(ctx->gen_done[b], ctx->stream));
         if (bounce) {
-            int rc = pump();  // the previous tile, while this one is being generated
-            if (rc) return rc;
-            pend = {b, dst, dpitch, spitch, width, rows, true};
+            inflight[b] = ctx->lanes->post(ctx->d_stage[b], spitch, dst, dpitch, width, rows, ctx->gen_done[b]);
             return MK2_OK;
         }
         CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[b], 0));
@@ -617,68 +645,27 @@ public:
     int finish()
     {
         if (bounce) {
-            int rc = pump();
-            if (rc) return rc;
+            int rc;
+            const int last = (int)((count + 1) & 1);  // older tile first
+            if ((rc = reclaim(last ^ 1)) || (rc = reclaim(last))) return rc;
+            return MK2_OK;
         }
         return drain_copies(ctx);
     }
 
 private:
-    struct Pending {
-        int b = 0;
-        uint8_t *dst = nullptr;
-        size_t dpitch = 0, spitch = 0, width = 0, rows = 0;
-        bool live = false;
-    };
-    // Move the pending tile out: staging buffer -> pinned slots (copy stream) -> caller's array (copy workers).
-    // Returns with the staging buffer free again, so the caller needs no stream-side wait before reusing it.
-    int pump()
+    int reclaim(int b)
     {
-        if (!pend.live) return MK2_OK;
-        pend.live = false;
-        const Pending t = pend;
-        CK(cudaStreamWaitEvent(ctx->copy, ctx->gen_done[t.b], 0));
-        // sub-chunks: whole rows (narrow rows) or pieces of one row (rows wider than a slot)
-        const size_t rows_per_sub = std::max<size_t>(1, BOUNCE_BYTES / t.width);
-        const size_t cols_per_sub = t.width <= BOUNCE_BYTES ? t.width : BOUNCE_BYTES;
-        const size_t col_subs = (t.width + cols_per_sub - 1) / cols_per_sub;
-        const size_t row_subs = (t.rows + rows_per_sub - 1) / rows_per_sub;
-        const size_t nsub = row_subs * col_subs;
-        const uint8_t *src = static_cast<const uint8_t *>(ctx->d_stage[t.b]);
-        uint8_t *ring = static_cast<uint8_t *>(ctx->h_bounce);
-        auto geom = [&](size_t i, size_t &r0, size_t &nr, size_t &c0, size_t &nc) {
-            r0 = (i / col_subs) * rows_per_sub;
-            nr = std::min(rows_per_sub, t.rows - r0);
-            c0 = (i % col_subs) * cols_per_sub;
-            nc = std::min(cols_per_sub, t.width - c0);
-        };
-        size_t issued = 0, done = 0;
-        while (done < nsub) {
-            while (issued < nsub && issued - done < (size_t)BOUNCE_SLOTS) {
-                size_t r0, nr, c0, nc;
-                geom(issued, r0, nr, c0, nc);
-                const int slot = (int)(issued % BOUNCE_SLOTS);
-                uint8_t *h = ring + (size_t)slot * BOUNCE_BYTES;
-                if (t.spitch == nc)
-                    CK(cudaMemcpyAsync(h, src + r0 * t.spitch, nc * nr, cudaMemcpyDeviceToHost, ctx->copy));
-                else
-                    CK(cudaMemcpy2DAsync(h, nc, src + r0 * t.spitch + c0, t.spitch, nc, nr, cudaMemcpyDeviceToHost, ctx->copy));
-                CK(cudaEventRecord(ctx->sub_done[slot], ctx->copy));
-                ++issued;
-            }
-            size_t r0, nr, c0, nc;
-            geom(done, r0, nr, c0, nc);
-            const int slot = (int)(done % BOUNCE_SLOTS);
-            CK(cudaEventSynchronize(ctx->sub_done[slot]));
-            ctx->copy_pool->copy2d(t.dst + r0 * t.dpitch + c0, t.dpitch, ring + (size_t)slot * BOUNCE_BYTES, nc, nc, nr);
-            ++done;
-        }
+        if (!inflight[b]) return MK2_OK;
+        const int e = ctx->lanes->wait(inflight[b]);
+        inflight[b].reset();
+        if (e) return fail(ctx, MK2_E_CUDA, std::string("copy lane: ") + cudaGetErrorString((cudaError_t)e));
         return MK2_OK;
     }
     mk2_ctx *ctx;
     bool bounce;
     uint64_t count = 0;
-    Pending pend;
+    HostCopyLanes::TilePtr inflight[2];
 };
 
 int check_ready(mk2_ctx *ctx)
@@ -822,8 +809,8 @@ int mk2_destroy(mk2_ctx *ctx)
 {
     if (!ctx) return MK2_OK;
     DeviceGuard guard(ctx->device);
-    delete ctx->copy_pool;
-    ctx->copy_pool = nullptr;
+    delete ctx->lanes;
+    ctx->lanes = nullptr;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->copy) cudaStreamSynchronize(ctx->copy);
     if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
@@ -835,9 +822,6 @@ int mk2_destroy(mk2_ctx *ctx)
         if (ctx->gen_done[b]) cudaEventDestroy(ctx->gen_done[b]);
         if (ctx->copy_done[b]) cudaEventDestroy(ctx->copy_done[b]);
     }
-    if (ctx->h_bounce) cudaFreeHost(ctx->h_bounce);
-    for (auto &e : ctx->sub_done)
-        if (e) cudaEventDestroy(e);
     if (ctx->d_state) cudaFree(ctx->d_state);
     if (ctx->d_acc) cudaFree(ctx->d_acc);
     if (ctx->d_sum) cudaFree(ctx->d_sum);
@@ -960,8 +944,8 @@ int mk2_set_host_threads(mk2_ctx *ctx, int threads)
     if (!ctx) return MK2_E_ARG;
     if (threads < 0 || threads > 256) return fail(ctx, MK2_E_ARG, "host threads must be 0 (automatic) or 1..256");
     if (threads != ctx->host_threads) {
-        delete ctx->copy_pool;  // idle between calls; re-created with the new size on next use
-        ctx->copy_pool = nullptr;
+        delete ctx->lanes;  // idle between calls; re-created with the new size on next use
+        ctx->lanes = nullptr;
         ctx->host_threads = threads;
     }
     return MK2_OK;
@@ -1339,7 +1323,7 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
         for (uint64_t t0 = 0; t0 < T; t0 += chunk) {
             const uint64_t tc = std::min(chunk, T - t0);
             const int b = tiles.next();
-            if ((rc = acquire_stage(ctx, b))) return rc;
+            if ((rc = tiles.acquire(b))) return rc;
             if ((rc = launch_col(ctx, tc, static_cast<uint32_t *>(ctx->d_stage[b]), ctx->G))) return rc;
             uint8_t *dst = static_cast<uint8_t *>(out) + t0 * stride_words * sizeof(uint32_t);
             if ((rc = tiles.copy_out(b, dst, stride_words * sizeof(uint32_t), row_bytes, row_bytes, tc))) return rc;
@@ -1380,7 +1364,7 @@ static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pit
             const uint64_t tc = std::min(tc_max, T - t0);
             const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
             const int b = tiles.next();
-            if ((rc = acquire_stage(ctx, b))) return rc;
+            if ((rc = tiles.acquire(b))) return rc;
             if ((rc = launch_row(ctx, tc, static_cast<uint8_t *>(ctx->d_stage[b]), sp, c0, nch))) return rc;
             if ((rc = tiles.copy_out(b, out + row0 * pitch_bytes + t0 / 8, pitch_bytes, sp, tc / 8, nrows))) return rc;
         }
