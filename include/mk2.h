@@ -20,14 +20,14 @@
  *   pinned host      (cudaHostAlloc / cudaHostRegister / mk2_host_alloc /
  *                    torch pin_memory) outputs receive asynchronous D2H copies
  *                    of the device staging tiles directly, at link speed;
- *   pageable host    (malloc, a fresh numpy array) outputs of 8 MiB or more are
+ *   pageable host    (malloc, a fresh numpy array) outputs of 64 MiB or more are
  *                    moved by the context's copy lanes (mk2_set_host_threads):
- *                    host threads with their own stream and 4 MiB page-locked
- *                    slot that each copy sub-chunks of the device staging tile
- *                    to the slot and memcpy them into the caller's array, so
- *                    several D2H copies are in flight while others are being
- *                    moved; smaller outputs and pageable inputs (key/IV bytes,
- *                    20 B per instance) are plain cudaMemcpyAsync calls.
+ *                    host threads with their own stream and two page-locked
+ *                    slots that each copy sub-chunks (2 or 8 MiB) of the device
+ *                    staging tile to a slot and move the previous one into the
+ *                    caller's array meanwhile, so several D2H copies are always
+ *                    in flight; smaller outputs and pageable inputs (key/IV
+ *                    bytes, 20 B per instance) are plain cudaMemcpyAsync calls.
  * Every output call returns with the caller's array complete.
  *
  * Current device: every entry point runs on its context's device and restores
@@ -233,7 +233,7 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
  * row-major tiles, which are 2-D copies, are 16x this). */
 int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes);
 /* Number of copy lanes (host threads) that move staging tiles into PAGEABLE
- * output arrays; 0 = automatic (one per hardware thread, 2..16). */
+ * output arrays; 0 = automatic (three quarters of the hardware threads, 2..12). */
 int mk2_set_host_threads(mk2_ctx *ctx, int threads);
 /* Pinned (page-locked, portable) host memory for output arrays that should take
  * the direct D2H path: what the Python front end's fresh result arrays are made

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -34,7 +35,7 @@ thread_local std::string g_create_error;  // text of this thread's last failed m
 constexpr size_t STAGE_BYTES = size_t(32) << 20;
 constexpr size_t ROW_TILE_FACTOR = 16;
 // Pageable host outputs below this size are left to the driver's own staged copy (no lanes, no page-locking).
-constexpr uint64_t BOUNCE_MIN_BYTES = uint64_t(8) << 20;
+constexpr uint64_t BOUNCE_MIN_BYTES = uint64_t(64) << 20;
 
 // Restores the caller's current device when an entry point returns: a process that drives torch on cuda:0 and
 // an mk2 context on device 1 keeps its own current device.
@@ -61,14 +62,54 @@ struct DeviceGuard {
 // Host side of PAGEABLE output buffers.  A D2H copy into pageable memory is staged by the driver
 // through its own small pinned buffers on the calling thread (measured on this box: 10-13 GB/s against
 // 56 GB/s into pinned memory).  Here a few independent COPY LANES do it in parallel: a lane is a host
-// thread with its own CUDA stream, event and page-locked slot.  A device staging tile is cut into
-// sub-chunks of LANE_BYTES; every lane repeatedly claims the next sub-chunk, copies it device -> slot on
-// its stream, waits for it and memcpy's the slot into the caller's array (a fresh numpy array takes its
-// first-touch page faults there, spread over the lanes).  While one lane is in memcpy the others have
-// their D2H copies in flight, so the link stays busy; tiles are queued, so the lanes run on into the
-// next tile while the calling thread is launching kernels.
+// thread with its own CUDA stream, two events and two page-locked slots.  A device staging tile is cut
+// into sub-chunks of LANE_BYTES; every lane repeatedly claims the next sub-chunk, starts its device ->
+// slot copy on its stream, and meanwhile memcpy's the sub-chunk that landed in its other slot into the
+// caller's array (a fresh numpy array takes its first-touch page faults there, spread over the lanes).
+// The link stays busy with the lanes' copies; tiles are queued, so the lanes run on into the next tile
+// while the calling thread is launching kernels.
 // ---------------------------------------------------------------------------
-constexpr size_t LANE_BYTES = size_t(4) << 20;
+// Sub-chunk size and store flavour, measured on the 16-core B200 host with 2 GiB outputs
+// (profiles/r02_probe_copy_lanes.txt; pinned destination: 56.5 GB/s column-major, 51 GB/s row-major):
+//   contiguous destination (column-major tiles): 8 MiB sub-chunks moved with non-temporal stores 51 GB/s from
+//       8 lanes on; 2 MiB sub-chunks 46 GB/s with plain memcpy, 36 GB/s with non-temporal stores;
+//   pitched destination (row-major tiles, 1 KiB row pieces): 2 MiB sub-chunks 46 GB/s at 16 lanes (either
+//       store flavour), 8 MiB sub-chunks 36 GB/s.
+constexpr size_t LANE_BYTES_WIDE = size_t(8) << 20;
+constexpr size_t LANE_BYTES_PITCHED = size_t(2) << 20;
+
+#if defined(__x86_64__) && defined(__GNUC__)
+#include <immintrin.h>
+// memcpy with non-temporal stores: the destination (the caller's result array) is written once and not read
+// back by these threads, so the lines need not be fetched for ownership nor kept in cache.
+__attribute__((target("avx2"))) void stream_copy(uint8_t *dst, const uint8_t *src, size_t n)
+{
+    const size_t head = (32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31;
+    if (n < 4096 || head > n) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::memcpy(dst, src, head);
+    dst += head; src += head; n -= head;
+    size_t i = 0;
+    for (; i + 128 <= n; i += 128) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 32));
+        const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 64));
+        const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 96));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 96), d);
+    }
+    _mm_sfence();
+    std::memcpy(dst + i, src + i, n - i);
+}
+bool cpu_has_avx2() { return __builtin_cpu_supports("avx2"); }
+#else
+void stream_copy(uint8_t *dst, const uint8_t *src, size_t n) { std::memcpy(dst, src, n); }
+bool cpu_has_avx2() { return false; }
+#endif
 
 class HostCopyLanes {
 public:
@@ -80,6 +121,8 @@ public:
         size_t rows_per_sub = 1, cols_per_sub = 1, col_subs = 1, nsub = 0;
         std::atomic<size_t> next{0};
         std::atomic<size_t> remaining{0};
+        size_t sub_bytes = 0;          // page-locked slot space one sub-chunk needs
+        bool nt = false;               // move it with non-temporal stores
         std::atomic<int> error{0};     // first cudaError_t seen by a lane
         unsigned long long id = 0;     // never reused (a freed tile's address can be)
     };
@@ -87,6 +130,10 @@ public:
 
     HostCopyLanes(int device, int nlanes) : device_(device)
     {
+        // experiment knobs (tools/probe_lanes.py): sub-chunk size and store flavour of the lanes
+        if (const char *v = std::getenv("MK2_LANE_BYTES")) lane_bytes_ = std::max<size_t>(65536, std::strtoull(v, nullptr, 0));
+        avx2_ = cpu_has_avx2();
+        if (const char *v = std::getenv("MK2_LANE_NT")) nt_override_ = std::atoi(v) != 0 ? 1 : 0;
         for (int i = 0; i < nlanes; ++i) lanes_.emplace_back([this] { run(); });
     }
     ~HostCopyLanes()
@@ -106,8 +153,12 @@ public:
         t->dst = static_cast<uint8_t *>(dst);
         t->spitch = spitch; t->dpitch = dpitch; t->width = width; t->rows = rows; t->ready = ready;
         // sub-chunks: whole rows (narrow rows) or pieces of one row (rows wider than a slot)
-        t->rows_per_sub = std::max<size_t>(1, LANE_BYTES / width);
-        t->cols_per_sub = std::min(width, LANE_BYTES);
+        const bool wide = dpitch == width;  // the tile is one contiguous run in the caller's array
+        const size_t lane_bytes = lane_bytes_ ? lane_bytes_ : (wide ? LANE_BYTES_WIDE : LANE_BYTES_PITCHED);
+        t->nt = avx2_ && (nt_override_ >= 0 ? nt_override_ != 0 : wide);
+        t->rows_per_sub = std::max<size_t>(1, lane_bytes / width);
+        t->cols_per_sub = std::min(width, lane_bytes);
+        t->sub_bytes = t->rows_per_sub * t->cols_per_sub;
         t->col_subs = (width + t->cols_per_sub - 1) / t->cols_per_sub;
         t->nsub = ((rows + t->rows_per_sub - 1) / t->rows_per_sub) * t->col_subs;
         t->remaining.store(t->nsub);
@@ -130,66 +181,128 @@ public:
     }
 
 private:
-    void run()
+    struct Sub {
+        TilePtr t;
+        size_t r0 = 0, nr = 0, c0 = 0, nc = 0;
+        int slot = 0;
+        cudaError_t e = cudaSuccess;
+    };
+    // Next unclaimed sub-chunk of the oldest unfinished tile; with `block` it sleeps until there is one (or the
+    // lanes are shut down), without it returns false at once when the queue is empty.
+    bool claim(bool block, Sub &s)
     {
-        cudaStream_t stream = nullptr;
-        cudaEvent_t ev = nullptr;
-        void *slot = nullptr;
-        bool ok = cudaSetDevice(device_) == cudaSuccess &&
-                  cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
-                  cudaHostAlloc(&slot, LANE_BYTES, cudaHostAllocDefault) == cudaSuccess;
-        unsigned long long synced = 0;  // id of the tile whose `ready` event this lane's stream already waits on
         for (;;) {
             TilePtr t;
             {
                 std::unique_lock<std::mutex> lk(m_);
                 for (;;) {
                     while (!queue_.empty() && queue_.front()->next.load() >= queue_.front()->nsub) queue_.pop_front();
-                    if (stop_ || !queue_.empty()) break;
+                    if (stop_ || !queue_.empty() || !block) break;
                     cv_.wait(lk);
                 }
-                if (stop_) break;
+                if (stop_ || queue_.empty()) return false;
                 t = queue_.front();
             }
             const size_t i = t->next.fetch_add(1);
             if (i >= t->nsub) continue;
-            cudaError_t e = ok ? cudaSuccess : cudaErrorInitializationError;
-            const size_t r0 = (i / t->col_subs) * t->rows_per_sub, nr = std::min(t->rows_per_sub, t->rows - r0);
-            const size_t c0 = (i % t->col_subs) * t->cols_per_sub, nc = std::min(t->cols_per_sub, t->width - c0);
-            if (e == cudaSuccess && synced != t->id) {
-                e = cudaStreamWaitEvent(stream, t->ready, 0);
-                synced = t->id;
-            }
+            s.r0 = (i / t->col_subs) * t->rows_per_sub;
+            s.nr = std::min(t->rows_per_sub, t->rows - s.r0);
+            s.c0 = (i % t->col_subs) * t->cols_per_sub;
+            s.nc = std::min(t->cols_per_sub, t->width - s.c0);
+            s.t = std::move(t);
+            return true;
+        }
+    }
+    void run()
+    {
+        // a lane = this thread, one stream, two page-locked slots: the D2H copy of its next sub-chunk is in flight
+        // while it moves the current one into the caller's array
+        cudaStream_t stream = nullptr;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        void *slots = nullptr;   // two page-locked slots of slot_bytes each, grown to the largest sub-chunk seen
+        size_t slot_bytes = 0;
+        const bool ok = cudaSetDevice(device_) == cudaSuccess &&
+                        cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) == cudaSuccess &&
+                        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) == cudaSuccess &&
+                        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) == cudaSuccess;
+        unsigned long long synced = 0;  // id of the tile whose `ready` event this lane's stream already waits on
+        Sub cur, nxt;
+        bool have_cur = false;
+        auto land = [&] {  // wait for the current sub-chunk's D2H copy and move it into the caller's array
+            Tile &t = *cur.t;
+            cudaError_t e = cur.e;
+            if (e == cudaSuccess) e = cudaEventSynchronize(ev[cur.slot]);
             if (e == cudaSuccess) {
-                if (t->spitch == nc)
-                    e = cudaMemcpyAsync(slot, t->src + r0 * t->spitch, nc * nr, cudaMemcpyDeviceToHost, stream);
-                else
-                    e = cudaMemcpy2DAsync(slot, nc, t->src + r0 * t->spitch + c0, t->spitch, nc, nr, cudaMemcpyDeviceToHost, stream);
-            }
-            if (e == cudaSuccess) e = cudaEventRecord(ev, stream);
-            if (e == cudaSuccess) e = cudaEventSynchronize(ev);
-            if (e == cudaSuccess) {
-                uint8_t *d = t->dst + r0 * t->dpitch + c0;
-                const uint8_t *h = static_cast<const uint8_t *>(slot);
-                if (t->dpitch == nc) std::memcpy(d, h, nc * nr);
-                else
-                    for (size_t r = 0; r < nr; ++r) std::memcpy(d + r * t->dpitch, h + r * nc, nc);
+                uint8_t *d = t.dst + cur.r0 * t.dpitch + cur.c0;
+                const uint8_t *h = static_cast<const uint8_t *>(slots) + (size_t)cur.slot * slot_bytes;
+                if (!t.nt) {
+                    if (t.dpitch == cur.nc) std::memcpy(d, h, cur.nc * cur.nr);
+                    else
+                        for (size_t r = 0; r < cur.nr; ++r) std::memcpy(d + r * t.dpitch, h + r * cur.nc, cur.nc);
+                } else if (t.dpitch == cur.nc) {
+                    stream_copy(d, h, cur.nc * cur.nr);
+                } else {
+                    for (size_t r = 0; r < cur.nr; ++r) stream_copy(d + r * t.dpitch, h + r * cur.nc, cur.nc);
+                }
             } else {
                 int zero = 0;
-                t->error.compare_exchange_strong(zero, (int)e);
+                t.error.compare_exchange_strong(zero, (int)e);
                 cudaGetLastError();
             }
-            if (t->remaining.fetch_sub(1) == 1) {
+            if (t.remaining.fetch_sub(1) == 1) {
                 std::lock_guard<std::mutex> lk(m_);
                 done_.notify_all();
             }
+            cur.t.reset();
+            have_cur = false;
+        };
+        for (;;) {
+            const bool have_nxt = claim(!have_cur, nxt);
+            if (!have_nxt && !have_cur) break;  // shut down (a blocking claim only fails on stop)
+            if (have_nxt) {
+                Tile &t = *nxt.t;
+                cudaError_t e = ok ? cudaSuccess : cudaErrorInitializationError;
+                if (t.sub_bytes > slot_bytes) {  // larger slots needed: nothing may be in flight in the old ones
+                    if (have_cur) land();
+                    if (slots) cudaFreeHost(slots);
+                    slots = nullptr;
+                    slot_bytes = 0;
+                    if (e == cudaSuccess) e = cudaHostAlloc(&slots, 2 * t.sub_bytes, cudaHostAllocDefault);
+                    if (e == cudaSuccess) slot_bytes = t.sub_bytes;
+                }
+                // start its D2H copy into the slot `cur` does not use
+                nxt.slot = have_cur ? cur.slot ^ 1 : 0;
+                uint8_t *h = static_cast<uint8_t *>(slots) + (size_t)nxt.slot * slot_bytes;
+                if (e == cudaSuccess && synced != t.id) {
+                    e = cudaStreamWaitEvent(stream, t.ready, 0);
+                    synced = t.id;
+                }
+                if (e == cudaSuccess) {
+                    if (t.spitch == nxt.nc)
+                        e = cudaMemcpyAsync(h, t.src + nxt.r0 * t.spitch, nxt.nc * nxt.nr, cudaMemcpyDeviceToHost, stream);
+                    else
+                        e = cudaMemcpy2DAsync(h, nxt.nc, t.src + nxt.r0 * t.spitch + nxt.c0, t.spitch, nxt.nc, nxt.nr,
+                                              cudaMemcpyDeviceToHost, stream);
+                }
+                if (e == cudaSuccess) e = cudaEventRecord(ev[nxt.slot], stream);
+                nxt.e = e;
+            }
+            if (have_cur) land();
+            if (have_nxt) {
+                cur = std::move(nxt);
+                have_cur = true;
+                nxt = Sub{};
+            }
         }
-        if (slot) cudaFreeHost(slot);
-        if (ev) cudaEventDestroy(ev);
+        if (slots) cudaFreeHost(slots);
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
     int device_;
+    size_t lane_bytes_ = 0;   // 0 = by tile shape
+    bool avx2_ = false;
+    int nt_override_ = -1;
     std::vector<std::thread> lanes_;
     std::mutex m_;
     std::condition_variable cv_, done_;
@@ -220,6 +333,7 @@ struct mk2_ctx {
     uint32_t chunk_user = 0;             // user override of clocks per scheduling chunk (0 = automatic)
     int block_user = 0;                  // user override of threads per persistent CTA (0 = automatic)
     size_t stage_target = STAGE_BYTES;   // bytes per host-output staging tile (mk2_set_stage_bytes)
+    bool stage_user = false;             // ... set by the caller (honoured as is for pageable outputs too)
     int row_staging = 0;                 // row-major staging tile: 0 = automatic, 1 = shared memory, 2 = tensor memory
     int last_plan_block = 0;
     uint32_t last_plan_chunk = 0;
@@ -366,10 +480,11 @@ int ensure_lanes(mk2_ctx *ctx)
     if (ctx->lanes) return MK2_OK;
     int n = ctx->host_threads;
     if (n <= 0) {
-        // every core up to 16 (profiles/r02_probe_host_buffers.txt: the lanes alternate between waiting for their
-        // D2H copy and memcpy, so more lanes than memcpy alone would need keep the link busy)
+        // three quarters of the hardware threads, 2..12 (profiles/r02_probe_copy_lanes.txt, 16-core host: contiguous
+        // tiles peak at 8-12 lanes and lose 10% at 16, when the lanes compete with the driver's own threads;
+        // pitched row tiles keep gaining up to 16)
         const unsigned hw = std::thread::hardware_concurrency();
-        n = (int)std::min<unsigned>(16u, std::max<unsigned>(2u, hw));
+        n = (int)std::min<unsigned>(12u, std::max<unsigned>(2u, hw * 3 / 4));
     }
     ctx->lanes = new (std::nothrow) HostCopyLanes(ctx->device, n);
     if (!ctx->lanes) return fail(ctx, MK2_E_NOMEM, "out of host memory");
@@ -618,6 +733,7 @@ public:
         if (bounce && ctx->lanes)
             for (auto &t : inflight) ctx->lanes->wait(t);
     }
+    bool pageable() const { return bounce; }
     int prepare() { return bounce ? ensure_lanes(ctx) : MK2_OK; }
     int next() { return (int)(count++ & 1); }
     int acquire(int b)
@@ -924,6 +1040,7 @@ int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes)
     if (!ctx) return MK2_E_ARG;
     if (bytes && bytes < (1u << 20)) return fail(ctx, MK2_E_ARG, "stage bytes must be 0 (default) or at least 1 MiB");
     ctx->stage_target = bytes ? (size_t)bytes : STAGE_BYTES;
+    ctx->stage_user = bytes != 0;
     return MK2_OK;
 }
 
@@ -1315,9 +1432,12 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
         // stream while the next tile is generated.  Pinned destinations take the D2H copy directly; pageable
         // ones go through the pinned bounce buffers and the copy workers (HostTiles).
         const size_t row_bytes = ctx->G * sizeof(uint32_t);
-        const size_t want = std::max<size_t>(std::min<size_t>(ctx->stage_target, T * row_bytes), row_bytes);
-        if ((rc = ensure_stage(ctx, want))) return rc;
         HostTiles tiles(ctx, mem, T * row_bytes);
+        // copy lanes work on 8 MiB sub-chunks: give them tiles of at least 128 MiB to spread over
+        const size_t target = tiles.pageable() && !ctx->stage_user ? std::max<size_t>(ctx->stage_target, size_t(128) << 20)
+                                                                    : ctx->stage_target;
+        const size_t want = std::max<size_t>(std::min<size_t>(target, T * row_bytes), row_bytes);
+        if ((rc = ensure_stage(ctx, want))) return rc;
         if ((rc = tiles.prepare())) return rc;
         const uint64_t chunk = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
         for (uint64_t t0 = 0; t0 < T; t0 += chunk) {
@@ -1346,9 +1466,13 @@ static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pit
     // tile = [block_chains x 1024 rows] x [tc_max clocks] of about ROW_TILE_FACTOR x stage_target bytes, rows at
     // least 512 B wide when T allows (narrower 2-D copies collapse: 192 B rows 37 GB/s, 64 B rows 16 GB/s), and
     // between one and two chains per worker warp of a full launch
+    // Pageable destinations: the copy lanes memcpy row pieces into the caller's pitched array, and 512-byte pieces
+    // move at two thirds of the rate of 1 KiB ones (profiles/r02_probe_host_buffers.txt), so rows are 1 KiB wide
+    // and the chain block is halved instead (half the worker warps still generate at twice the link rate).
+    const bool pageable = tiles.pageable();
     const uint64_t tile_bytes = ROW_TILE_FACTOR * ctx->stage_target;
-    const uint64_t min_clocks = std::min<uint64_t>((T + 255) / 256 * 256, 4096);
-    const uint64_t workers = 8ull * (uint64_t)ctx->sm_count;
+    const uint64_t min_clocks = std::min<uint64_t>((T + 255) / 256 * 256, pageable ? 8192 : 4096);
+    const uint64_t workers = (pageable ? 4ull : 8ull) * (uint64_t)ctx->sm_count;
     const uint64_t want_chains = std::min<uint64_t>(2 * workers, std::max<uint64_t>(workers, tile_bytes / (min_clocks / 8) / 1024));
     const uint64_t block_chains = std::min<uint64_t>(chains, want_chains);
     const uint64_t block_rows = block_chains * 1024;

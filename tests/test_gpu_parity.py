@@ -1133,13 +1133,13 @@ def test_pageable_host_outputs_go_through_bounce_tiles(pkg, oracle):
     """Caller-owned PAGEABLE numpy arrays (what kernels.py:194-200 returns) large enough for the pinned bounce
     pipeline: several staging tiles per call, column-major (contiguous and strided), row-major (pitched) and the
     one-shot bulk call -- all bit-exact against the oracle; the pool-backed default arrays agree."""
-    N, T = 16384 + 96, 4096
+    N, T = (1 << 17) + 96, 4096                                        # 64 MiB per layout: the copy lanes' threshold
     keys, ivs = random_arrays(77, N)
     want_c = oracle.bulk_colmajor(keys, ivs, 80, T)
     want_r = oracle.bulk_rowmajor(keys, ivs, 80, T)
     G = (N + 31) // 32
     with pkg.MickeyGenerator(0) as gen:
-        gen.set_stage_bytes(1 << 20)                                   # 8 MiB of output = 8 column tiles
+        gen.set_stage_bytes(5 << 20)                                   # 13 column tiles, several row tiles
         gen.set_host_threads(3)
         out = np.empty((T, G), np.uint32)                              # pageable, first touched by the copy workers
         gen.init_material(keys, ivs, 80).generate_colmajor(T, out)
