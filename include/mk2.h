@@ -244,7 +244,9 @@ int mk2_host_free(void *p);
 /* Tuning knob: where the row-major kernel parks 256 keystream words per thread
  * between two drains: 1 = shared memory (seven worker warps per SM fit),
  * 2 = tensor memory (tcgen05.st / tcgen05.ld; eight fit), 0 = automatic
- * (tensor memory).  MICKEY only: the Grain kernels always use shared memory. */
+ * (tensor memory).  Grain v1: 0 and 1 = 256-clock tiles in shared memory;
+ * 2 = the experimental 512-clock tiles split between tensor and shared memory
+ * (64 contiguous bytes per row and drain; slower overall). */
 int mk2_set_row_staging(mk2_ctx *ctx, int mode);
 int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 

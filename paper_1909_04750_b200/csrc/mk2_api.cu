@@ -22,6 +22,7 @@
 #include "mk2_kernels.cuh"
 #include "mk2_tmem.cuh"
 #include "mk2_grain.cuh"
+#include "mk2_grain_row64.cuh"
 #include "mk2_seedgen.cuh"
 
 using namespace mk2;
@@ -549,6 +550,7 @@ struct Plan {
     uint32_t cpc;     // chunks per chain
     unsigned grid;
     bool tmem;        // row-major only: staging tile in tensor memory (mk2_tmem.cuh)
+    bool row64;       // Grain row-major: 512-clock tiles, 64 bytes per row and drain (mk2_grain_row64.cuh)
 };
 
 Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
@@ -561,6 +563,15 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
     p.tmem = rowmajor && ctx->cipher == 0 && ctx->row_staging != 1;
     p.block = ctx->block_user ? ctx->block_user : (chains >= 16 * sms ? (rowmajor && !p.tmem ? 224 : 256) : 128);
     p.tg = p.tmem || p.block <= 224 ? 32 : 16;  // smem strides: <= 128 -> 128, <= 192 -> 192, <= 224 -> 224, else (16, 256)
+    // Grain row-major with mk2_set_row_staging(ctx, 2): 512-clock tiles (64 contiguous bytes per row and drain),
+    // four in tensor memory and three and a half in shared memory.  NOT the default: it takes DRAM out of the
+    // picture (17% busy instead of the limiter) but its staging instructions cost what that returns
+    // (9.9-10.1 Tb/s against 10.4 for the 256-clock shared-memory kernel, Grain section).
+    p.row64 = rowmajor && ctx->cipher == 1 && ctx->row_staging == 2 && !ctx->block_user;
+    if (p.row64) {
+        p.block = grain::row64::THREADS;
+        p.tg = grain::row64::NGRP;
+    }
     const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::WIN : 1u);
     auto round_chunk = [&](uint64_t c) {
         c = std::max<uint64_t>(c, granule);
@@ -641,6 +652,19 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     const Plan p = make_plan(ctx, T, true, nchains);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
+    if (p.row64) {
+        if (ctx->row_lsb)
+            grain::row64::gen_rowmajor_kernel<true><<<p.grid, p.block, grain::row64::SMEM_BYTES, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base, aligned);
+        else
+            grain::row64::gen_rowmajor_kernel<false><<<p.grid, p.block, grain::row64::SMEM_BYTES, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base, aligned);
+        CK(cudaGetLastError());
+        ctx->last_launches++;
+        return MK2_OK;
+    }
     // staging geometry: (TG, stride) = (32, 128) | (32, 192) | (32, 224) | (16, 256); the stride is a template
     // parameter so that every smem offset in the drain loops is an immediate
     const int ts = p.tg == 32 ? (p.block <= 128 ? 128 : p.block <= 192 ? 192 : 224) : 256;
@@ -831,6 +855,12 @@ cudaError_t opt_in_row_kernels(int device)
     MK2_OPT_IN_GRAIN(32, 224);
     MK2_OPT_IN_GRAIN(16, 256);
 #undef MK2_OPT_IN_GRAIN
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grain::row64::gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 grain::row64::SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grain::row64::gen_rowmajor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 grain::row64::SMEM_BYTES);
     if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
     return e;
 }

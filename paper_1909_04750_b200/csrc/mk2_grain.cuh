@@ -41,9 +41,10 @@ constexpr unsigned L_AXORB_AND_C = 0x28; // (a ^ b) & c
 //   h = A ^ x2 D with A = x1 ^ x4 ^ t, t = x3 (x0 ^ x4), D = t ^ x3 ^ MAJ(x0, x1, x4)   (Shannon on x2)
 //   g = 12 linear taps ^ P1..P11 with the shared pairs b63b60, b37b33, b15b9, b52b45, b28b21; products
 //       of three or more taps are reduced to a pair and folded in as acc ^ (p & q).
-template <int C, bool INIT>
-__device__ __forceinline__ uint32_t step(uint32_t (&b)[GW], uint32_t (&s)[GW])
+template <int C, bool INIT, int NW>
+__device__ __forceinline__ uint32_t step(uint32_t (&b)[NW], uint32_t (&s)[NW])
 {
+    static_assert(C + GB < NW, "window too short for this offset");
     // ---- output z (grain.py:127-133)
     const uint32_t x0 = s[C + 3], x1 = s[C + 25], x2 = s[C + 46], x3 = s[C + 64], x4 = b[C + 63];
     const uint32_t t = lop3<L_AXORB_AND_C>(x0, x4, x3);
@@ -91,8 +92,8 @@ __device__ __forceinline__ uint32_t step(uint32_t (&b)[GW], uint32_t (&s)[GW])
     return z;
 }
 
-template <int N>
-__device__ __forceinline__ void realign(uint32_t (&b)[GW], uint32_t (&s)[GW])
+template <int N, int NW>
+__device__ __forceinline__ void realign(uint32_t (&b)[NW], uint32_t (&s)[NW])
 {
 #pragma unroll
     for (int i = 0; i < GB; ++i) {
@@ -111,8 +112,9 @@ __device__ __forceinline__ void static_for_up(F &&f)
 }
 
 // state[160][G]: words 0..79 = NFSR, 80..159 = LFSR (same coalesced layout as MICKEY's)
+template <int NW>
 __device__ __forceinline__ void load_state(const uint32_t *state, const unsigned long long *acc, uint64_t G, uint64_t g,
-                                           uint32_t (&b)[GW], uint32_t (&s)[GW], unsigned long long &a)
+                                           uint32_t (&b)[NW], uint32_t (&s)[NW], unsigned long long &a)
 {
     const uint32_t *p = state + g;
 #pragma unroll
@@ -127,8 +129,9 @@ __device__ __forceinline__ void load_state(const uint32_t *state, const unsigned
     }
     a = __ldcg(acc + g);
 }
+template <int NW>
 __device__ __forceinline__ void store_state(uint32_t *state, unsigned long long *acc, uint64_t G, uint64_t g,
-                                            const uint32_t (&b)[GW], const uint32_t (&s)[GW], unsigned long long a)
+                                            const uint32_t (&b)[NW], const uint32_t (&s)[NW], unsigned long long a)
 {
     const uint32_t *p = state + g;
 #pragma unroll

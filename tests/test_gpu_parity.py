@@ -885,6 +885,35 @@ def test_grain_bulk_vs_oracle(pkg, oracle, block, chunk, torch_cuda):
     assert np.array_equal(dev.cpu().numpy(), oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb"))
 
 
+@pytest.mark.parametrize("N,T,chunk", [(32 * 70 + 11, 1000, 0), (1 << 15, 4096 + 520, 1024), (64, 8, 0), (4099, 136, 0)])
+def test_grain_rowmajor_512_clock_tiles(pkg, oracle, N, T, chunk, torch_cuda):
+    """The opt-in Grain row-major kernel with 512-clock tiles split between tensor and shared memory
+    (mk2_set_row_staging(ctx, 2); csrc/mk2_grain_row64.cuh): whole tiles, short tails, partial last groups,
+    both byte orders, unaligned rows -- same bytes as the oracle and as the default kernel."""
+    from paper_1909_04750_b200 import grain
+
+    rng = np.random.default_rng(N + T)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 8), dtype=np.uint8)
+    want = oracle.grain_bulk_rowmajor(keys, ivs, T)
+    with grain.GrainGenerator(0) as gen:
+        gen.set_row_staging(2)
+        gen.set_chunk_clocks(chunk)
+        row = gen.init_material(keys, ivs).generate_rowmajor(T)
+        csum = gen.checksum()
+        lsb = gen.init_material(keys, ivs).generate_rowmajor(T, bit_order="lsb")
+        dev = torch_cuda.zeros((N, T // 8 + 3), dtype=torch_cuda.uint8, device="cuda")   # pitch not a multiple of 16
+        gen.init_material(keys, ivs).generate_rowmajor(T, dev)
+        torch_cuda.cuda.synchronize()
+        assert gen.last_plan()[0] == 256
+        gen.set_row_staging(0)
+        ref = gen.init_material(keys, ivs).generate_rowmajor(T)
+        assert gen.checksum() == csum
+    assert np.array_equal(row, want) and np.array_equal(ref, want)
+    assert np.array_equal(lsb, oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb"))
+    assert np.array_equal(dev.cpu().numpy()[:, : T // 8], want)
+
+
 def test_grain_large_sampled(pkg, oracle, torch_cuda):
     """2^20 Grain instances x 4096 bits: sampled groups vs the oracle, layout-independent checksum."""
     from paper_1909_04750_b200 import grain

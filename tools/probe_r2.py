@@ -133,7 +133,37 @@ def hostbuf():
     out["host_buffers_2GiB"] = res
 
 
-for name, fn in (("ragged", ragged), ("latency", latency), ("hostbuf", hostbuf)):
+def e2e():
+    """bench.py's e2e_pageable leg in isolation: pageable key/IV arrays in + one 2 GiB pageable output per step,
+    by number of copy lanes; the pinned variant of the same step for comparison."""
+    import torch
+    N, T = 1 << 20, 16384
+    key = bytes.fromhex("123456789abcdef01234")
+    keys = np.tile(np.frombuffer(key, np.uint8), (N, 1))
+    ivs = np.zeros((N, 10), np.uint8)
+    ivs[:, 2:] = np.arange(N, dtype=np.uint64).astype(">u8").view(np.uint8).reshape(N, 8)
+    res = {}
+    with pkg.MickeyGenerator(0) as gen:
+        pk, pi = torch.from_numpy(keys).pin_memory(), torch.from_numpy(ivs).pin_memory()
+        pinned = torch.empty((T, N // 32), dtype=torch.int32).pin_memory()
+        step = lambda: (gen.init_material(pk, pi, 80), gen.generate_colmajor(T, pinned))
+        step()
+        res["pinned_ms"] = best(step, 4)[0] * 1e3
+        page = np.empty((T, N // 32), np.uint32)
+        for th in (6, 8, 10, 12, 14, 16):
+            gen.set_host_threads(th)
+            step = lambda: (gen.init_material(keys, ivs, 80), gen.generate_colmajor(T, page))
+            step()
+            b, med = best(step, 5)
+            res[f"pageable_lanes{th}_ms"] = {"best": b * 1e3, "median": med * 1e3}
+        gen.set_host_threads(0)
+        t0 = time.perf_counter()
+        gen.init_material(keys, ivs, 80)
+        res["init_from_pageable_inputs_ms"] = (time.perf_counter() - t0) * 1e3
+    out["e2e_pageable_leg"] = res
+
+
+for name, fn in (("ragged", ragged), ("latency", latency), ("hostbuf", hostbuf), ("e2e", e2e)):
     if len(sys.argv) < 2 or name in sys.argv[1:]:
         try:
             fn()
