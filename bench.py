@@ -667,8 +667,8 @@ def run_e2e(env: Env, n, clocks, layout, first):
                     the full `clocks` as resumable calls of --e2e-clocks bits into a ring of two pinned buffers
                     (the consumer owns one while the next fills); row-major is the one-shot mk2_bulk_rowmajor.
       e2e_pageable  the reference's calling convention (kernels.py:189-200): ordinary (pageable) numpy key/IV
-                    arrays in, numpy keystream out -- into a caller-supplied pageable array (pinned bounce tiles
-                    + copy workers inside the library) and into the fresh result array the package returns
+                    arrays in, numpy keystream out -- into a caller-supplied pageable array (the library's copy
+                    lanes) and into the fresh result array the package returns
                     (page-locked block from its pool).  Bounded sample: one --e2e-clocks call per step."""
     args, np, torch, pkg, gen = env.args, env.np, env.torch, env.pkg, env.gen
     world = env.world
@@ -695,6 +695,38 @@ def run_e2e(env: Env, n, clocks, layout, first):
         torch.cuda.synchronize()
         return env.max_over_ranks(time.perf_counter() - t0) / reps
 
+    # ---- pageable numpy in / numpy out (bounded sample: one call of tc bits per step)
+    res = {"unit": "Tb/s", "h2d_bytes_per_step": int(keys_np.nbytes + ivs_np.nbytes), "d2h_bytes_per_step": int(n * tc // 8),
+           "steps": steps}
+    if layout == "colmajor":
+        pinned_one = torch.empty((tc, G), dtype=torch.int32).pin_memory()
+        dt_pin = timed(lambda: (gen.init_material(keys, ivs, 80), gen.generate_colmajor(tc, pinned_one)), steps)
+        del pinned_one
+        page = np.empty((tc, G), np.uint32)
+        dt_page = timed(lambda: (gen.init_material(keys_np, ivs_np, 80), gen.generate_colmajor(tc, page)), steps)
+        del page
+        dt_fresh = timed(lambda: pkg.bulk_colmajor(keys_np, ivs_np, 80, tc, device=env.local), steps, warm=2)
+        calls = ("caller-supplied pageable array: mk2_init_from_material + mk2_generate_colmajor",
+                 "pkg.bulk_colmajor(keys, ivs, 80, T) returning a fresh array")
+    else:
+        pinned_one = torch.empty((n, tc // 8), dtype=torch.uint8).pin_memory()
+        dt_pin = timed(lambda: gen.bulk_rowmajor(keys, ivs, 80, tc, pinned_one), steps)
+        del pinned_one
+        page = np.empty((n, tc // 8), np.uint8)
+        dt_page = timed(lambda: gen.bulk_rowmajor(keys_np, ivs_np, 80, tc, page), steps)
+        del page
+        dt_fresh = timed(lambda: pkg.bulk_rowmajor(keys_np, ivs_np, 80, tc, device=env.local), steps, warm=2)
+        calls = ("caller-supplied pageable array: mk2_bulk_rowmajor", "pkg.bulk_rowmajor(keys, ivs, 80, T) returning a fresh array")
+    bits = world * n * tc
+    res.update({
+        "value": bits / dt_page / 1e12, "ms_per_step": dt_page * 1e3, "d2h_gb_s": n * tc / 8 / dt_page / 1e9,
+        "fresh_result_array": {"value": bits / dt_fresh / 1e12, "ms_per_step": dt_fresh * 1e3, "call": calls[1],
+                               "note": "the package's result arrays are page-locked blocks from a cached pool (hostmem.py)"},
+        "pinned_same_sample": {"value": bits / dt_pin / 1e12, "ms_per_step": dt_pin * 1e3},
+        "pageable_over_pinned": dt_pin / dt_page, "fresh_over_pinned": dt_pin / dt_fresh,
+        "workload": f"{n} of {n_full} instances x {tc} bits per GPU per call, pageable numpy key/IV arrays in; value = "
+                    + calls[0] + " (copy lanes inside the library: host threads with their own stream and page-locked slots)",
+    })
     # ---- pinned, whole length
     if layout == "colmajor":
         ring = [torch.empty((tc, G), dtype=torch.int32).pin_memory() for _ in range(2)]
@@ -735,38 +767,6 @@ def run_e2e(env: Env, n, clocks, layout, first):
                     + how + "; the host link, not the kernel, bounds it",
     }
 
-    # ---- pageable numpy in / numpy out (bounded sample: one call of tc bits per step)
-    res = {"unit": "Tb/s", "h2d_bytes_per_step": int(keys_np.nbytes + ivs_np.nbytes), "d2h_bytes_per_step": int(n * tc // 8),
-           "steps": steps}
-    if layout == "colmajor":
-        pinned_one = torch.empty((tc, G), dtype=torch.int32).pin_memory()
-        dt_pin = timed(lambda: (gen.init_material(keys, ivs, 80), gen.generate_colmajor(tc, pinned_one)), steps)
-        del pinned_one
-        page = np.empty((tc, G), np.uint32)
-        dt_page = timed(lambda: (gen.init_material(keys_np, ivs_np, 80), gen.generate_colmajor(tc, page)), steps)
-        del page
-        dt_fresh = timed(lambda: pkg.bulk_colmajor(keys_np, ivs_np, 80, tc, device=env.local), steps, warm=2)
-        calls = ("caller-supplied pageable array: mk2_init_from_material + mk2_generate_colmajor",
-                 "pkg.bulk_colmajor(keys, ivs, 80, T) returning a fresh array")
-    else:
-        pinned_one = torch.empty((n, tc // 8), dtype=torch.uint8).pin_memory()
-        dt_pin = timed(lambda: gen.bulk_rowmajor(keys, ivs, 80, tc, pinned_one), steps)
-        del pinned_one
-        page = np.empty((n, tc // 8), np.uint8)
-        dt_page = timed(lambda: gen.bulk_rowmajor(keys_np, ivs_np, 80, tc, page), steps)
-        del page
-        dt_fresh = timed(lambda: pkg.bulk_rowmajor(keys_np, ivs_np, 80, tc, device=env.local), steps, warm=2)
-        calls = ("caller-supplied pageable array: mk2_bulk_rowmajor", "pkg.bulk_rowmajor(keys, ivs, 80, T) returning a fresh array")
-    bits = world * n * tc
-    res.update({
-        "value": bits / dt_page / 1e12, "ms_per_step": dt_page * 1e3, "d2h_gb_s": n * tc / 8 / dt_page / 1e9,
-        "fresh_result_array": {"value": bits / dt_fresh / 1e12, "ms_per_step": dt_fresh * 1e3, "call": calls[1],
-                               "note": "the package's result arrays are page-locked blocks from a cached pool (hostmem.py)"},
-        "pinned_same_sample": {"value": bits / dt_pin / 1e12, "ms_per_step": dt_pin * 1e3},
-        "pageable_over_pinned": dt_pin / dt_page, "fresh_over_pinned": dt_pin / dt_fresh,
-        "workload": f"{n} of {n_full} instances x {tc} bits per GPU per call, pageable numpy key/IV arrays in; value = "
-                    + calls[0] + " (pinned bounce tiles + copy workers inside the library)",
-    })
     gen.set_async(True)
     return e2e, res
 

@@ -233,7 +233,8 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks);
  * row-major tiles, which are 2-D copies, are 16x this). */
 int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes);
 /* Number of copy lanes (host threads) that move staging tiles into PAGEABLE
- * output arrays; 0 = automatic (three quarters of the hardware threads, 2..12). */
+ * output arrays; 0 = automatic (one per hardware thread, 2..16; contiguous
+ * column-major tiles use at most 8 of them). */
 int mk2_set_host_threads(mk2_ctx *ctx, int threads);
 /* Pinned (page-locked, portable) host memory for output arrays that should take
  * the direct D2H path: what the Python front end's fresh result arrays are made

@@ -126,6 +126,7 @@ public:
         bool nt = false;               // move it with non-temporal stores
         std::atomic<int> error{0};     // first cudaError_t seen by a lane
         unsigned long long id = 0;     // never reused (a freed tile's address can be)
+        int lanes_wanted = 1 << 30;    // lanes with a higher index leave this tile to the others
     };
     using TilePtr = std::shared_ptr<Tile>;
 
@@ -135,7 +136,8 @@ public:
         if (const char *v = std::getenv("MK2_LANE_BYTES")) lane_bytes_ = std::max<size_t>(65536, std::strtoull(v, nullptr, 0));
         avx2_ = cpu_has_avx2();
         if (const char *v = std::getenv("MK2_LANE_NT")) nt_override_ = std::atoi(v) != 0 ? 1 : 0;
-        for (int i = 0; i < nlanes; ++i) lanes_.emplace_back([this] { run(); });
+        lanes_override_ = std::getenv("MK2_LANE_ALL") != nullptr;
+        for (int i = 0; i < nlanes; ++i) lanes_.emplace_back([this, i] { run(i); });
     }
     ~HostCopyLanes()
     {
@@ -157,6 +159,9 @@ public:
         const bool wide = dpitch == width;  // the tile is one contiguous run in the caller's array
         const size_t lane_bytes = lane_bytes_ ? lane_bytes_ : (wide ? LANE_BYTES_WIDE : LANE_BYTES_PITCHED);
         t->nt = avx2_ && (nt_override_ >= 0 ? nt_override_ != 0 : wide);
+        // contiguous tiles are at their best with 6-8 lanes (8 MiB non-temporal sub-chunks saturate the memory
+        // system; more lanes only compete), pitched row tiles keep gaining up to 16 (profiles/r02_probe_copy_lanes.txt)
+        if (wide && !lanes_override_) t->lanes_wanted = 8;
         t->rows_per_sub = std::max<size_t>(1, lane_bytes / width);
         t->cols_per_sub = std::min(width, lane_bytes);
         t->sub_bytes = t->rows_per_sub * t->cols_per_sub;
@@ -190,7 +195,7 @@ private:
     };
     // Next unclaimed sub-chunk of the oldest unfinished tile; with `block` it sleeps until there is one (or the
     // lanes are shut down), without it returns false at once when the queue is empty.
-    bool claim(bool block, Sub &s)
+    bool claim(bool block, Sub &s, int lane)
     {
         for (;;) {
             TilePtr t;
@@ -198,11 +203,17 @@ private:
                 std::unique_lock<std::mutex> lk(m_);
                 for (;;) {
                     while (!queue_.empty() && queue_.front()->next.load() >= queue_.front()->nsub) queue_.pop_front();
-                    if (stop_ || !queue_.empty() || !block) break;
+                    // the oldest unfinished tile this lane may work on
+                    t.reset();
+                    for (const auto &q : queue_)
+                        if (lane < q->lanes_wanted && q->next.load() < q->nsub) {
+                            t = q;
+                            break;
+                        }
+                    if (stop_ || t || !block) break;
                     cv_.wait(lk);
                 }
-                if (stop_ || queue_.empty()) return false;
-                t = queue_.front();
+                if (stop_ || !t) return false;
             }
             const size_t i = t->next.fetch_add(1);
             if (i >= t->nsub) continue;
@@ -214,7 +225,7 @@ private:
             return true;
         }
     }
-    void run()
+    void run(int lane)
     {
         // a lane = this thread, one stream, two page-locked slots: the D2H copy of its next sub-chunk is in flight
         // while it moves the current one into the caller's array
@@ -258,7 +269,7 @@ private:
             have_cur = false;
         };
         for (;;) {
-            const bool have_nxt = claim(!have_cur, nxt);
+            const bool have_nxt = claim(!have_cur, nxt, lane);
             if (!have_nxt && !have_cur) break;  // shut down (a blocking claim only fails on stop)
             if (have_nxt) {
                 Tile &t = *nxt.t;
@@ -304,6 +315,7 @@ private:
     size_t lane_bytes_ = 0;   // 0 = by tile shape
     bool avx2_ = false;
     int nt_override_ = -1;
+    bool lanes_override_ = false;
     std::vector<std::thread> lanes_;
     std::mutex m_;
     std::condition_variable cv_, done_;
@@ -481,11 +493,9 @@ int ensure_lanes(mk2_ctx *ctx)
     if (ctx->lanes) return MK2_OK;
     int n = ctx->host_threads;
     if (n <= 0) {
-        // three quarters of the hardware threads, 2..12 (profiles/r02_probe_copy_lanes.txt, 16-core host: contiguous
-        // tiles peak at 8-12 lanes and lose 10% at 16, when the lanes compete with the driver's own threads;
-        // pitched row tiles keep gaining up to 16)
+        // one lane per hardware thread, 2..16; a tile uses as many of them as suit its shape (HostCopyLanes::post)
         const unsigned hw = std::thread::hardware_concurrency();
-        n = (int)std::min<unsigned>(12u, std::max<unsigned>(2u, hw * 3 / 4));
+        n = (int)std::min<unsigned>(16u, std::max<unsigned>(2u, hw));
     }
     ctx->lanes = new (std::nothrow) HostCopyLanes(ctx->device, n);
     if (!ctx->lanes) return fail(ctx, MK2_E_NOMEM, "out of host memory");
