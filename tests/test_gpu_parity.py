@@ -1325,6 +1325,8 @@ def test_reference_shaped_calls_reuse_idle_contexts(pkg, golden):
     (cli.py:219-231) take an idle context of the thread instead of creating and destroying one per call."""
     from paper_1909_04750_b200 import hostmem
     from paper_1909_04750_b200.generator import MickeyGenerator
+    import gc
+    gc.collect()                          # engines of earlier tests still waiting for the collector release theirs now
     hostmem.drop_idle_contexts()
     rec = golden["kats"][0]
     mats = [pkg.MickeyKeyIv(bytes.fromhex(rec["key"]), bytes.fromhex(rec["iv"]))] * 64
