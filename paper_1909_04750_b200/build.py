@@ -53,7 +53,7 @@ def _stamp(target: Path, sources) -> None:
 
 def build_native(force: bool = False, verbose: bool = False) -> Path:
     """Compile libmk2.so (kernels + C ABI)."""
-    srcs = [*CSRC.glob("mk2_*.cuh"), CSRC / "mk2_api.cu", PKG.parent / "include" / "mk2.h"]
+    srcs = [*CSRC.glob("mk2_*.cuh"), *CSRC.glob("mk2_*.h"), CSRC / "mk2_api.cu", PKG.parent / "include" / "mk2.h"]
     if force or _stale(LIB, srcs):
         cmd = [nvcc(), *ARCH, *COMMON, "-Xptxas", "-v", "-o", str(LIB), str(CSRC / "mk2_api.cu"), "-lcudart"]
         res = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
