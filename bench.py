@@ -685,7 +685,7 @@ def run_e2e(env: Env, n, clocks, layout, first):
     steps = max(1, min(args.steps, 3))
     G = n // 32
 
-    def timed(fn, reps, warm=1):
+    def timed(fn, reps, warm=2):
         for _ in range(warm):
             fn()
         env.barrier()
@@ -742,7 +742,7 @@ def run_e2e(env: Env, n, clocks, layout, first):
                 done += c
                 i += 1
 
-        dt = timed(one, steps)
+        dt = timed(one, steps, warm=1)
         d2h = n * full_clocks // 8
         how = (f"mk2_init_from_material(pinned host keys, IVs) + {ncalls} resumable mk2_generate_colmajor calls of {tc} bits "
                f"into a ring of two pinned {tc * G * 4 >> 20} MiB host buffers")
