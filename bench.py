@@ -617,8 +617,10 @@ def run_ours(args):
     e2e = e2e_page = latency = None
     if not args.no_e2e:
         e2e, e2e_page = run_e2e(env, n, clocks, layout, first)
+    ragged = None
     if not args.no_latency and rank == 0:
         latency = small_call_latency(env)
+        ragged = ragged_init(env)
 
     line = None
     if rank == 0:
@@ -646,6 +648,8 @@ def run_ours(args):
             line["e2e_pageable"] = e2e_page
         if latency:
             line["small_call_latency"] = latency
+        if ragged:
+            line["ragged_init"] = ragged
         if not args.no_curand:
             try:
                 line["curand"] = curand_compare(torch, 1 << 32)
@@ -769,6 +773,34 @@ def run_e2e(env: Env, n, clocks, layout, first):
 
     gen.set_async(True)
     return e2e, res
+
+
+def ragged_init(env: Env) -> dict:
+    """Key/IV load + pre-clocks of 2^20 instances whose IV lengths differ (uniform over 0, 8, ..., 80 bits: the
+    reference's acceptance workload, tests/test_acceptance.py:103-135; mickey.py:287-289 gives such sets a per-lane
+    scalar init) against the uniform 80-bit init of the same instances.  Device-resident material; device time of
+    the packing + init kernels (mk2_last_kernel_ms), best of 5 after a warm-up call."""
+    np, torch, pkg = env.np, env.torch, env.pkg
+    n = 1 << 20
+    rng = np.random.default_rng(1)
+    keys = torch.from_numpy(rng.integers(0, 256, (n, 10), dtype=np.uint8)).to(env.dev)
+    ivs = torch.from_numpy(rng.integers(0, 256, (n, 10), dtype=np.uint8)).to(env.dev)
+    nb_bytes = torch.from_numpy((8 * rng.integers(0, 11, n)).astype(np.uint8)).to(env.dev)
+    nb_bits = torch.from_numpy(rng.integers(0, 81, n).astype(np.uint8)).to(env.dev)
+    with pkg.MickeyGenerator(env.local) as g:
+        def ms(fn):
+            v = []
+            for _ in range(6):
+                fn()
+                v.append(g.last_kernel_ms)
+            return min(v[1:])
+        uni = ms(lambda: g.init_material(keys, ivs, 80))
+        rb = ms(lambda: g.init_ragged(keys, ivs, nb_bytes))
+        rbit = ms(lambda: g.init_ragged(keys, ivs, nb_bits))
+    return {"instances": n, "uniform_80bit_ms": uni, "ragged_iv_0_to_10_bytes_ms": rb, "ragged_iv_0_to_80_bits_ms": rbit,
+            "ragged_over_uniform": rb / uni,
+            "note": "pack_ragged_kernel (128-bit loads, funnel shifts, 32x32 bit transposes) + init_kernel<true> (masked "
+                    "4-clock blocks, +5 LOP3 per IV clock); ragged includes the D2H of the 1 MiB length array"}
 
 
 def small_call_latency(env: Env) -> dict:

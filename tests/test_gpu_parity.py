@@ -1198,6 +1198,26 @@ def test_pageable_host_outputs_go_through_bounce_tiles(pkg, oracle):
         assert np.array_equal(c, want_c) and hostmem.pool.allocs == allocs
 
 
+def test_pageable_outputs_with_rows_wider_than_a_lane_slot(pkg, oracle, monkeypatch):
+    """Copy lanes when one row of the staging tile is wider than a lane's page-locked slot (column-major output of
+    more than 16 M instances with the default 8 MiB sub-chunks): sub-chunks are then pieces of rows.  Forced here
+    at 2^19 instances by shrinking the sub-chunk size (MK2_LANE_BYTES, read when a context creates its lanes)."""
+    monkeypatch.setenv("MK2_LANE_BYTES", "65536")
+    N, T = (1 << 19) + 64, 1024                                        # 65 544-byte rows, 64 MiB of output
+    key = bytes.fromhex("123456789abcdef01234")
+    G = N // 32
+    with pkg.MickeyGenerator(0) as gen:
+        out = np.empty((T, G), np.uint32)
+        gen.init_counter(key, 0, N).generate_colmajor(T, out)
+        csum = gen.checksum()
+        wide = np.zeros((T, G + 3), np.uint32)
+        gen.init_counter(key, 0, N).generate_colmajor(T, wide, stride_words=G + 3)
+    assert int(out.view("<u8").sum(dtype=np.uint64)) == csum == oracle.checksum_counter(key, 0, N, T)
+    assert np.array_equal(wide[:, :G], out) and not wide[:, G:].any()
+    keys, ivs = oracle.counter_material(key, 64 * 4000, 64)
+    assert np.array_equal(out[:, 8000:8002], oracle.bulk_colmajor(keys, ivs, 80, T))
+
+
 def test_rowmajor_lsb_bit_order(pkg, oracle):
     """bit_order="lsb" of words_to_lane_bytes / words_lane_major_bytes (kernels.py:604-621) straight from the GPU:
     the tensor-memory kernel, the shared-memory kernel, ragged tails and the host mirror's helpers agree."""
