@@ -318,6 +318,23 @@ def derive_material(seed: bytes, first_lane: int, n: int, tag: int = ALGO_TAG_MI
     return keys, ivs
 
 
+def suite_streams(seed: bytes, nstreams: int, stream_bits: int) -> np.ndarray:
+    """Restates cli._suite_streams (cli.py:212-231): batches of 64 lanes, batch b keyed by the master seed with its
+    first byte XORed with b, lane material from derive_lane_material, MSB-first packed keystream per lane (a last
+    partial byte zero-padded, as np.packbits does).  uint8[nstreams][ceil(stream_bits / 8)]."""
+    keys = np.zeros((nstreams, 10), np.uint8)
+    ivs = np.zeros((nstreams, 10), np.uint8)
+    for b in range((nstreams + 63) // 64):
+        lanes = min(64, nstreams - 64 * b)
+        k, v = derive_material(bytes([seed[0] ^ b]) + seed[1:], 0, lanes)
+        keys[64 * b: 64 * b + lanes], ivs[64 * b: 64 * b + lanes] = k, v
+    nbytes = (stream_bits + 7) // 8
+    rows = bulk_rowmajor(keys, ivs, 80, 8 * nbytes)
+    if stream_bits % 8:
+        rows[:, -1] &= np.uint8((0xFF << (8 - stream_bits % 8)) & 0xFF)
+    return rows
+
+
 # ---------------------------------------------------------------- Grain v1 (grain.py)
 
 def _grain_arrays(materials):

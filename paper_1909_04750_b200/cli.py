@@ -4,6 +4,10 @@
                                             [--interleave lane|bit] [--format hex|raw] [--out FILE]
     python -m paper_1909_04750_b200.cli vectors [--file F]
     python -m paper_1909_04750_b200.cli bench [--mib M] [--repeats R] [--lanes-log2 K] [--json-out F]
+    python -m paper_1909_04750_b200.cli streams --out DIR|FILE.npy [--seed HEX] [--streams N] [--stream-bits B]
+
+`streams` writes exactly the streams `slicerng test` generates for its NIST suite (cli.py:212-231), so that the
+reference's `slicerng test <files>` can judge GPU output.
 
 Same arguments, output order and exit codes as `slicerng gen/vectors/bench`
 for `--algo mickey` (pkg/src/slicerng/cli.py:102-152, 173-190, 296-369): lane-major
@@ -19,13 +23,14 @@ from __future__ import annotations
 import argparse
 import json
 import logging
+import os
 import statistics
 import sys
 import time
 
 import numpy as np
 
-from . import vectors
+from . import hostmem, vectors
 from .generator import MickeyGenerator
 from .grain import GrainGenerator, GrainKeyIv
 from .mickey import MickeyKeyIv
@@ -174,6 +179,50 @@ def measure(nbytes: int, lanes: int, warmup: int = 1, repeats: int = 5, device: 
             "gbit_per_s": total * 8 / seconds / 1e9, "runs": runs, "speedup_vs_naive": None}
 
 
+def suite_streams(seed: bytes, nstreams: int, stream_bits: int, device: int = 0) -> np.ndarray:
+    """The streams the reference's `slicerng test` feeds to its NIST suite (cli._suite_streams, cli.py:212-231):
+    batches of 64 lanes, batch b keyed by the master seed with its first byte XORed with b, lane material from
+    derive_lane_material, one mickey_sliced_words call per batch, every lane's bits packed MSB-first.  Here all
+    streams come from ONE init + row-major generation on the GPU (the per-batch seeds are derived on the GPU too).
+    Returns uint8[nstreams][ceil(stream_bits / 8)]; like np.packbits, a last partial byte is zero-padded."""
+    if len(seed) != 32:
+        raise ValueError("master seed must be 32 bytes")
+    if nstreams < 1 or stream_bits < 1:
+        raise ValueError("need at least one stream of at least one bit")
+    nbatches = (nstreams + 63) // 64
+    if nbatches > 256:
+        raise ValueError("at most 256 batches of 64 streams: the batch index is folded into one seed byte (cli.py:222)")
+    keys = np.empty((nstreams, 10), np.uint8)
+    ivs = np.empty((nstreams, 10), np.uint8)
+    nbytes = (stream_bits + 7) // 8
+    with hostmem.borrow_context(MickeyGenerator, device) as gen:
+        for b in range(nbatches):
+            lanes = min(64, nstreams - 64 * b)
+            batch_seed = bytes([seed[0] ^ b]) + seed[1:]
+            if batch_seed == bytes(32):
+                raise ValueError("all-zero master seed rejected")          # MasterSeed.__post_init__, seedgen.py:49-50
+            gen.derive_material(batch_seed, 0, lanes, keys[64 * b: 64 * b + lanes], ivs[64 * b: 64 * b + lanes])
+        rows, _ = gen.bulk_rowmajor(keys, ivs, 80, 8 * nbytes)
+    if stream_bits % 8:
+        rows[:, -1] &= np.uint8((0xFF << (8 - stream_bits % 8)) & 0xFF)      # np.packbits pads the tail with zeros
+    return rows
+
+
+def cmd_streams(args) -> int:
+    """Write the suite streams: one .npy (uint8[streams][bytes]) or one raw file per stream, ready for
+    `slicerng test <files>` (cli.py:183-198)."""
+    rows = suite_streams(_parse_hex(args.seed, 32, "seed"), args.streams, args.stream_bits, args.device)
+    if args.out.endswith(".npy"):
+        np.save(args.out, rows)
+    else:
+        os.makedirs(args.out, exist_ok=True)
+        for j, row in enumerate(rows):
+            with open(os.path.join(args.out, f"stream_{j:05d}.bin"), "wb") as fh:
+                fh.write(row.tobytes())
+    print(f"{rows.shape[0]} stream(s) of {args.stream_bits} bits written to {args.out}")
+    return EXIT_OK
+
+
 def cmd_bench(args) -> int:
     rec = measure(args.mib << 20, 1 << args.lanes_log2, repeats=args.repeats, device=args.device)
     print(f"{rec['algorithm']:8s} {rec['impl']:6s} lanes={rec['width']:<9d} {rec['nbytes'] / 2**20:10.1f} MiB "
@@ -210,6 +259,13 @@ def build_parser() -> argparse.ArgumentParser:
     v.add_argument("--file", help="vector file: key=<hex> iv=<hex> ks=<hex>")
     v.add_argument("--bit-order", choices=("msb", "lsb"), default="msb")
     v.set_defaults(func=cmd_vectors)
+
+    t = sub.add_parser("streams", help="generate the streams `slicerng test` would judge (same seeds, same lanes)")
+    t.add_argument("--seed", default="11" * 32)
+    t.add_argument("--streams", type=int, default=100)
+    t.add_argument("--stream-bits", type=int, default=1_000_000)
+    t.add_argument("--out", required=True, help="a .npy file, or a directory for one raw file per stream")
+    t.set_defaults(func=cmd_streams)
 
     b = sub.add_parser("bench", help="GPU keystream throughput in the reference's results schema")
     b.add_argument("--mib", type=int, default=4096)

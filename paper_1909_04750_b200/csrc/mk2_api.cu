@@ -1251,6 +1251,9 @@ static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pit
     const uint64_t block_rows = block_chains * 1024;
     uint64_t tc_max = std::max<uint64_t>(min_clocks, tile_bytes / block_rows / 32 * 256);
     tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
+    // a later block of a bulk call never needs larger staging buffers than the first one, but if it ever did the
+    // copy lanes must be done with the old buffers before they are replaced (ensure_stage only knows the streams)
+    if (block_rows * (tc_max / 8) > ctx->stage_bytes && (rc = tiles.finish())) return rc;
     if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
     if ((rc = tiles.prepare())) return rc;
     for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {

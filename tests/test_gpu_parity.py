@@ -1447,3 +1447,26 @@ def test_two_ranks_drive_the_gpu_and_allreduce_their_checksums(pkg, golden, orac
     with pkg.MickeyGenerator(0) as gen:                                # the same job on one context
         gen.init_counter(bytes.fromhex(key_hex), 0, n).generate_colmajor(T)
         assert gen.checksum() == want
+
+
+def test_suite_streams_match_the_reference_cli(pkg, oracle, tmp_path):
+    """`cli streams` / cli.suite_streams: the streams the reference's `slicerng test` would judge (cli.py:212-231),
+    all batches from one init + row-major generation on the GPU; digests made by the reference itself."""
+    import json
+    from pathlib import Path
+    from paper_1909_04750_b200 import cli
+    fx = json.loads((Path(__file__).resolve().parent / "golden" / "suite_streams_sha256.json").read_text())
+    for c in fx["cases"]:
+        rows = cli.suite_streams(bytes.fromhex(c["seed"]), c["streams"], c["stream_bits"])
+        assert rows.shape == (c["streams"], (c["stream_bits"] + 7) // 8)
+        assert [sha(r.tobytes()) for r in rows] == c["sha256"], c["seed"]
+    big = cli.suite_streams(bytes.fromhex("11" * 32), 1000, 8192)          # 16 batches, one GPU call
+    assert np.array_equal(big, oracle.suite_streams(bytes.fromhex("11" * 32), 1000, 8192))
+    out = tmp_path / "s.npy"
+    assert cli.main(["streams", "--streams", "5", "--stream-bits", "4096", "--out", str(out)]) == 0
+    assert np.array_equal(np.load(out), big[:5, :512])
+    d = tmp_path / "raw"
+    assert cli.main(["streams", "--streams", "3", "--stream-bits", "77", "--seed", "a7" + "00" * 31, "--out", str(d)]) == 0
+    assert sha((d / "stream_00002.bin").read_bytes()) == fx["cases"][3]["sha256"][2]
+    with pytest.raises(SystemExit):
+        cli.main(["streams", "--streams", "20000", "--stream-bits", "8", "--out", str(out)])   # > 256 batches

@@ -207,3 +207,16 @@ def test_whole_job_checksum_matches_reference_and_buffer_checksum(oracle, golden
     k = rng.integers(0, 256, (1000, 10), dtype=np.uint8)
     v = rng.integers(0, 256, (1000, 10), dtype=np.uint8)
     assert oracle.checksum_material(k, v, nb, 40) == oracle.checksum_colmajor(oracle.bulk_colmajor(k, v, nb, 40))
+
+
+def test_suite_streams_match_the_reference_cli(oracle):
+    """The streams `slicerng test` generates for its NIST suite (cli._suite_streams, cli.py:212-231), digests made
+    by the reference itself (oracle/gen_suite_streams.py): batch seeds, partial last batch, bit counts that are
+    not a multiple of 8."""
+    import json
+    from pathlib import Path
+    fx = json.loads((Path(__file__).resolve().parent / "golden" / "suite_streams_sha256.json").read_text())
+    for c in fx["cases"]:
+        rows = oracle.suite_streams(bytes.fromhex(c["seed"]), c["streams"], c["stream_bits"])
+        assert rows[0, :16].tobytes().hex() == c["first16"]
+        assert [sha(r.tobytes()) for r in rows] == c["sha256"], c["seed"]
