@@ -1369,22 +1369,15 @@ def test_reference_shaped_calls_reuse_idle_contexts(pkg, golden):
 
 
 def test_nist_rows_from_the_gpu_match_the_rows_the_suite_judged(pkg):
-    """Closes the chain of tests/test_nist_quality.py: the 100 x 1 Mbit rows on which the reference's NIST
-    SP 800-22 subset passes (instances 0, 256, ... of the counter-IV set) are, by SHA-256, exactly what the B200
-    emits row-major for those instances (stats.py:525-567, tests/test_acceptance.py:208-223)."""
+    """Closes the chain of tests/test_nist_quality.py: the 100 x 1 Mbit streams of the reference's acceptance
+    criterion 4 (test_acceptance.py:188-223), on which the reference's NIST SP 800-22 subset passes, are, by
+    SHA-256, exactly what the B200 emits for them (cli.suite_streams: seed-derived material, one row-major run)."""
     import json
     from pathlib import Path
-    import torch
+    from paper_1909_04750_b200 import cli
     fx = json.loads((Path(__file__).resolve().parent / "golden" / "nist_rows_sha256.json").read_text())
-    step, nrows, T = fx["instance_step"], fx["rows"], fx["nbits"]
-    N = step * nrows
-    with pkg.MickeyGenerator(0) as gen:
-        gen.init_counter(bytes.fromhex(fx["key"]), 0, N)
-        rows = torch.empty((N, T // 8), dtype=torch.uint8, device="cuda")
-        gen.generate_rowmajor(T, rows)
-        torch.cuda.synchronize()
-        sel = rows[::step].cpu().numpy()
-    assert [hashlib.sha256(r.tobytes()).hexdigest() for r in sel] == fx["sha256"]
+    rows = cli.suite_streams(bytes.fromhex(fx["seed"]), fx["rows"], fx["nbits"])
+    assert [hashlib.sha256(r.tobytes()).hexdigest() for r in rows] == fx["sha256"]
 
 
 def _gpu_rank_worker(rank, world, port, n, T, key_hex, q):
