@@ -6,7 +6,7 @@ lane-major byte layout, served by hand-written sm_100a CUDA kernels behind a
 C ABI (include/mk2.h).  No CPU fallback: importing works anywhere, generating
 needs a B200.
 """
-from . import grain, kernels, mickey, seedgen, sharding
+from . import grain, hostmem, kernels, mickey, seedgen, sharding
 from .generator import MickeyGenerator
 from .kernels import (
     bulk_colmajor,
@@ -27,5 +27,5 @@ __all__ = [
     "mickey_constants", "mickey_sliced_words", "bulk_colmajor", "bulk_rowmajor",
     "words_to_lane_bits", "words_to_lane_bytes", "words_lane_major_bytes",
     "GrainGenerator", "GrainKeyIv", "GrainKeyIvError", "GrainSliced", "grain_sliced_words",
-    "grain", "kernels", "mickey", "seedgen", "sharding",
+    "grain", "hostmem", "kernels", "mickey", "seedgen", "sharding",
 ]
