@@ -72,6 +72,11 @@ def parse_args():
                     help="other single-GPU configs measured in the same run as extra_workloads: 'auto' (the other two "
                          "at N=1 with the default workload), 'none', or a comma list of c2,c3,c5")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="process-group backend for N > 1.  nccl (default): one GPU per rank.  gloo: a debug mode that lets "
+                         "several ranks share the GPUs there are (rank r drives cuda:(r mod device count)); the collectives "
+                         "then carry CPU tensors.  It exists so that the whole N > 1 code path of this file runs on a "
+                         "one-GPU box (tests/test_gpu_parity.py); its throughput is not a multi-GPU figure.")
     ap.add_argument("--total-bits", type=float, default=8e12,
                     help="strong scaling: keystream bits of the whole job (BASELINE configs[3]: 1 TB = 8e12)")
     ap.add_argument("--instances-log2", type=int, default=None, help="override instances per GPU (log2)")
@@ -313,10 +318,17 @@ class Env:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         if not torch.cuda.is_available():
             raise SystemExit("bench.py: no CUDA device; the MICKEY path has no CPU fallback")
+        self.backend = args.dist_backend
+        if self.backend == "gloo":
+            self.local %= torch.cuda.device_count()
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
+        self.cdev = self.dev if self.backend == "nccl" else torch.device("cpu")   # where collective tensors live
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=self.dev)
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
         self.stream = torch.cuda.current_stream()
         self.lib = _native.lib()
         self.gen = pkg.MickeyGenerator(self.local)
@@ -327,20 +339,24 @@ class Env:
 
     def barrier(self):
         if self.world > 1:
-            self.dist.barrier(device_ids=[self.local])
+            self.torch.cuda.synchronize()
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[self.local])
+            else:
+                self.dist.barrier()
         self.torch.cuda.synchronize()
 
     def max_over_ranks(self, x: float) -> float:
         if self.world == 1:
             return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.cdev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def gather_rows(self, row):
         """One small float64/int64 row per rank -> list of rows on every rank (after the timed region)."""
         torch = self.torch
-        t = torch.tensor(row, dtype=torch.int64, device=self.dev)
+        t = torch.tensor(row, dtype=torch.int64, device=self.cdev)
         if self.world == 1:
             return [t.tolist()]
         out = [torch.empty_like(t) for _ in range(self.world)]
@@ -544,14 +560,14 @@ def checksum_crosscheck(env: Env, shards) -> dict:
 
     first, count = shards[env.rank]
     mine = slice_sum(first, count)
-    reduced = sharding.allreduce_checksum(mine, device=env.dev)
+    reduced = sharding.allreduce_checksum(mine, device=env.cdev)
     alone = 0
     if env.rank == 0:
         for f, c in shards:
             alone = (alone + slice_sum(f, c)) % (1 << 64)
     return {"slice": f"first {min(count, 2048)} instances of every rank x {T} bits", "allreduced": f"{reduced:#018x}",
             "single_rank_recomputation": f"{alone:#018x}", "equal": reduced == alone if env.rank == 0 else None,
-            "collective": "one int64 SUM all-reduce (NCCL)" if env.world > 1 else "none (world size 1)"}
+            "collective": f"one int64 SUM all-reduce ({env.backend})" if env.world > 1 else "none (world size 1)"}
 
 
 def run_ours(args):
@@ -582,7 +598,7 @@ def run_ours(args):
     value = bits_per_step * args.steps / (main["elapsed_ms"] * 1e-3) / 1e12
 
     # ---- per-rank record + the checksum all-reduce (the only exchange; outside the timed region)
-    csum = sharding.allreduce_checksum(main["checksum"], device=env.dev)
+    csum = sharding.allreduce_checksum(main["checksum"], device=env.cdev)
     rows = env.gather_rows([rank, first, n, int(round(main["local_ms"] * 1e3)), sharding.to_i64(main["checksum"])])
     ranks = [{"rank": r[0], "first": r[1], "count": r[2], "ms": r[3] / 1e3, "checksum": f"{sharding.from_i64(r[4]):#018x}"}
              for r in rows]
@@ -634,7 +650,9 @@ def run_ours(args):
                 "instances_per_gpu": n, "clocks": clocks, "layout": layout, "output": main["out_mode"],
                 "total_instances": total_n, "total_bits_per_step": bits_per_step,
                 "l2": f"no flush needed: each step streams {main['out_bytes'] / 1e9:.1f} GB of output per GPU (>> 126 MB L2)",
-                "parallelism": f"{world} x disjoint key/IV ranges ({args.scaling} scaling), no data-path collective",
+                "parallelism": f"{world} x disjoint key/IV ranges ({args.scaling} scaling), no data-path collective"
+                               + ("" if env.backend == "nccl" or world == 1 else
+                                  f"; DEBUG backend gloo: {world} ranks share {torch.cuda.device_count()} GPU(s), not a multi-GPU figure"),
             },
             "roofline": main["roofline"], "step_split": main["split"], "clocks": main["clocks_info"],
             "gpu_launches": main["launches"],
@@ -659,7 +677,7 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_sample(args.cpu_seconds)
     gen.close()
     if world > 1:
-        env.dist.barrier(device_ids=[local])
+        env.barrier()
         env.dist.destroy_process_group()
     if line:
         print(json.dumps(line), flush=True)

@@ -1463,3 +1463,42 @@ def test_suite_streams_match_the_reference_cli(pkg, oracle, tmp_path):
     assert sha((d / "stream_00002.bin").read_bytes()) == fx["cases"][3]["sha256"][2]
     with pytest.raises(SystemExit):
         cli.main(["streams", "--streams", "20000", "--stream-bits", "8", "--out", str(out)])   # > 256 batches
+
+
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_multi_rank_code_path_on_one_gpu(scaling):
+    """bench.py launched the way the driver launches it for N > 1 (torch.distributed.run, one process per rank),
+    with the gloo debug backend so that two ranks can share the one GPU: disjoint key/IV ranges per rank, per-rank
+    records, the all-reduced checksum and its in-run cross-check, weak and strong (fixed total job) scaling."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(root / "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--dist-backend", "gloo", "--clocks", "16384", "--no-e2e", "--no-curand", "--no-cpu-baseline", "--no-latency"]
+    cmd += ["--instances-log2", "16"] if scaling == "weak" else ["--scaling", "strong", "--total-bits", str(16384 * (3 * 32768 + 64))]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=str(root))
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]                          # rank 0 prints the one JSON line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["value"] > 0 and d["gpu_launches"] > 0
+    r0, r1 = d["ranks"]
+    assert (r0["rank"], r1["rank"]) == (0, 1) and r0["first"] == 0 and r1["first"] == r0["count"]
+    total = r0["count"] + r1["count"]
+    assert total == d["config"]["total_instances"] == (2 << 16 if scaling == "weak" else 3 * 32768 + 64)
+    assert d["checksum_check"]["equal"] is True and "gloo" in d["checksum_check"]["collective"]
+    csum = (int(r0["checksum"], 16) + int(r1["checksum"], 16)) % (1 << 64)
+    assert int(d["checksum_u64_sum"], 16) == csum
+    # the same job on one context gives the same checksum (the last timed step's key/IV ranges)
+    import paper_1909_04750_b200 as p
+    step = (2 + 3 - 1) % 4                                              # bench rotates 4 starting indices over its steps
+    with p.MickeyGenerator(0) as gen:
+        gen.init_counter(bytes.fromhex("123456789abcdef01234"), step * total, total).generate_colmajor(16384)
+        assert gen.checksum() == csum

@@ -150,7 +150,7 @@ def e2e():
         step()
         res["pinned_ms"] = best(step, 4)[0] * 1e3
         page = np.empty((T, N // 32), np.uint32)
-        for th in (6, 8, 10, 12, 14, 16):
+        for th in (0, 8, 0, 8, 6, 16):
             gen.set_host_threads(th)
             step = lambda: (gen.init_material(keys, ivs, 80), gen.generate_colmajor(T, page))
             step()
