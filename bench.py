@@ -86,6 +86,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-curand", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-ncu-traffic", action="store_true",
+                    help="do not measure roofline.traffic live (one launch of each workload under ncu in a child process)")
+    ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target size of the CPU sample")
     ap.add_argument("--cpu-kind", choices=("auto", "reference", "port"), default="auto",
                     help="--impl reference: the reference's own numba loop from oracle/_ref (auto: when importable), "
@@ -220,7 +223,7 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     rb, why = (None, "--cpu-kind port") if args.cpu_kind == "port" else reference_import()
     if rb is None and args.cpu_kind == "reference":
-        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        emit({"impl": "reference", "unavailable": why})
         return
     budget = 150.0  # seconds for the whole arm
     if rb is not None:
@@ -268,7 +271,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "Tb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -324,7 +327,10 @@ class Env:
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         self.cdev = self.dev if self.backend == "nccl" else torch.device("cpu")   # where collective tensors live
-        if self.world > 1:
+        # Under torchrun a process group exists even at world size 1, so that a one-GPU box still executes the
+        # NCCL-specific calls of the N > 1 path (init, barrier(device_ids), CUDA-tensor collectives).
+        self.grouped = self.world > 1 or ("RANK" in os.environ and "MASTER_ADDR" in os.environ)
+        if self.grouped:
             if self.backend == "nccl":
                 dist.init_process_group("nccl", device_id=self.dev)
             else:
@@ -338,7 +344,7 @@ class Env:
         self.lop3_peak = None
 
     def barrier(self):
-        if self.world > 1:
+        if self.grouped:
             self.torch.cuda.synchronize()
             if self.backend == "nccl":
                 self.dist.barrier(device_ids=[self.local])
@@ -347,7 +353,7 @@ class Env:
         self.torch.cuda.synchronize()
 
     def max_over_ranks(self, x: float) -> float:
-        if self.world == 1:
+        if not self.grouped:
             return x
         t = self.torch.tensor([x], dtype=self.torch.float64, device=self.cdev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
@@ -357,7 +363,7 @@ class Env:
         """One small float64/int64 row per rank -> list of rows on every rank (after the timed region)."""
         torch = self.torch
         t = torch.tensor(row, dtype=torch.int64, device=self.cdev)
-        if self.world == 1:
+        if not self.grouped:
             return [t.tolist()]
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t)
@@ -567,7 +573,8 @@ def checksum_crosscheck(env: Env, shards) -> dict:
             alone = (alone + slice_sum(f, c)) % (1 << 64)
     return {"slice": f"first {min(count, 2048)} instances of every rank x {T} bits", "allreduced": f"{reduced:#018x}",
             "single_rank_recomputation": f"{alone:#018x}", "equal": reduced == alone if env.rank == 0 else None,
-            "collective": f"one int64 SUM all-reduce ({env.backend})" if env.world > 1 else "none (world size 1)"}
+            "collective": f"one int64 SUM all-reduce ({env.backend}, world size {env.world})" if env.grouped
+                          else "none (no process group: single process)"}
 
 
 def run_ours(args):
@@ -638,6 +645,16 @@ def run_ours(args):
         latency = small_call_latency(env)
         ragged = ragged_init(env)
 
+    # ---- roofline.traffic, live: DRAM bytes of one launch of every measured workload, counted by ncu in a child
+    # process (default geometry only; the parent has released its output buffers by now)
+    default_geometry = args.instances_log2 is None and args.clocks is None and args.scaling == "weak"
+    if rank == 0 and not env.grouped and not args.no_ncu_traffic and default_geometry:
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        apply_live_traffic(main["roofline"], args.workload)
+        for w in extras:
+            apply_live_traffic(extras[w]["roofline"], w)
+
     line = None
     if rank == 0:
         line = {
@@ -676,11 +693,11 @@ def run_ours(args):
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_sample(args.cpu_seconds)
     gen.close()
-    if world > 1:
+    if env.grouped:
         env.barrier()
         env.dist.destroy_process_group()
     if line:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def run_e2e(env: Env, n, clocks, layout, first):
@@ -881,8 +898,105 @@ def small_call_latency(env: Env) -> dict:
             "overhead_over_kernel_time_excluding_python_packing_us": pooled[0] - min(kern) * 1e3 - pack_us}
 
 
+def traffic_child(args):
+    """Child of measure_traffic_live: two launches of the workload's keystream kernel at its exact geometry (ncu
+    skips the first and counts the DRAM bytes of the second).  Nothing is timed here."""
+    import torch
+
+    import paper_1909_04750_b200 as pkg
+
+    lg, clocks, layout, _cfg = WORKLOADS[args.workload]
+    n = 1 << lg
+    dev = torch.device("cuda", 0)
+    with pkg.MickeyGenerator(0) as gen:
+        if args.workload == "c5":
+            g = torch.Generator(device=dev).manual_seed(0x190904750)
+            d_keys = torch.randint(0, 256, (n, 10), dtype=torch.uint8, device=dev, generator=g)
+            d_ivs = torch.randint(0, 256, (n, 10), dtype=torch.uint8, device=dev, generator=g)
+        out = (torch.empty((clocks, n // 32), dtype=torch.int32, device=dev) if layout == "colmajor"
+               else torch.empty((n, clocks // 8), dtype=torch.uint8, device=dev))
+        for _ in range(2):
+            if args.workload == "c5":
+                gen.init_material(d_keys, d_ivs, 80)
+            else:
+                gen.init_counter(KEY, 0, n)
+            gen.generate_colmajor(clocks, out) if layout == "colmajor" else gen.generate_rowmajor(clocks, out)
+        torch.cuda.synchronize()
+
+
+def measure_traffic_live(workload: str, timeout_s: float = 300.0):
+    """roofline.traffic measured in THIS run: dram__bytes_read.sum + dram__bytes_write.sum of one launch of the
+    workload's keystream kernel at its full geometry, counted by ncu around a child process of this script (a
+    number taken under a profiler is never a timing; DRAM byte counts are what the profiler is for).
+    Returns (bytes, source) or (None, reason)."""
+    import csv
+    import io
+    import shutil
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return None, "ncu not found"
+    layout = WORKLOADS[workload][2]
+    kern = "gen_colmajor_kernel" if layout == "colmajor" else "gen_rowmajor_kernel"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--print-units", "base",
+           "--csv", "-k", f"regex:{kern}", "--launch-skip", "1", "--launch-count", "1",
+           sys.executable, str(Path(__file__).resolve()), "--traffic-child", "--workload", workload]
+    try:
+        res = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, timeout=timeout_s, cwd=str(ROOT))
+    except (OSError, subprocess.TimeoutExpired) as exc:
+        return None, f"ncu child failed: {exc!r}"[:200]
+    start = res.stdout.find('"ID"')
+    if res.returncode != 0 or start < 0:
+        tail = (res.stdout + res.stderr).strip().splitlines()[-1:] or ["no output"]
+        return None, f"ncu child rc={res.returncode}: {tail[0]}"[:200]
+    total, seen = 0, 0
+    for row in csv.DictReader(io.StringIO(res.stdout[start:])):
+        if row.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += int(float(row["Metric Value"].replace(",", "")))
+            seen += 1
+    if seen != 2:
+        return None, "ncu output without the two DRAM counters"
+    return total, ("measured in this run: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none around "
+                   f"a child process of bench.py, one {kern} launch of exactly this geometry (second of two)")
+
+
+def apply_live_traffic(roofline: dict, workload: str):
+    live, src = measure_traffic_live(workload)
+    roofline["traffic_committed_profile"] = {"bytes": roofline.get("traffic"), "source": roofline.get("traffic_source")}
+    if live is not None:
+        roofline["traffic"], roofline["traffic_source"] = live, src
+        alg = roofline.get("algorithmic_bytes_per_launch")
+        roofline["traffic_over_algorithmic"] = live / alg if alg else None
+    else:
+        roofline["traffic_live_unavailable"] = src
+
+
+_JSON_OUT = None
+
+
+def claim_stdout():
+    """stdout must carry exactly ONE JSON line, but libraries write there too (NCCL prints its version banner to
+    stdout when NCCL_DEBUG is set, numba and ncu children may warn): keep a private handle on the real stdout for
+    the line and point file descriptor 1 at stderr for everybody else."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
     args = parse_args()
+    claim_stdout()
+    if args.traffic_child:
+        traffic_child(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

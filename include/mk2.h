@@ -247,7 +247,10 @@ int mk2_host_free(void *p);
  * 2 = tensor memory (tcgen05.st / tcgen05.ld; eight fit), 0 = automatic
  * (tensor memory).  Grain v1: 0 and 1 = 256-clock tiles in shared memory;
  * 2 = the experimental 512-clock tiles split between tensor and shared memory
- * (64 contiguous bytes per row and drain; slower overall). */
+ * (64 contiguous bytes per row and drain; slower overall);
+ * 3 = the same 512-clock tiles in global scratch meant to stay in L2 (74 MB;
+ * measured: it does not stay, 7.2 Tb/s against 10.4 -- kept as a documented
+ * negative result).  Mode 3 on a MICKEY context behaves like 0. */
 int mk2_set_row_staging(mk2_ctx *ctx, int mode);
 int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 

@@ -80,7 +80,9 @@ struct mk2_ctx {
     int block_user = 0;                  // user override of threads per persistent CTA (0 = automatic)
     size_t stage_target = STAGE_BYTES;   // bytes per host-output staging tile (mk2_set_stage_bytes)
     bool stage_user = false;             // ... set by the caller (honoured as is for pageable outputs too)
-    int row_staging = 0;                 // row-major staging tile: 0 = automatic, 1 = shared memory, 2 = tensor memory
+    int row_staging = 0;                 // row-major staging tile: 0 = automatic, 1 = shared memory, 2 = tensor memory,
+                                         // 3 = L2-resident scratch (Grain only)
+    uint32_t *d_rowscratch = nullptr;    // staging mode 3: one 64 KiB tile per worker warp (lazy)
     int last_plan_block = 0;
     uint32_t last_plan_chunk = 0;
     Trace trace = {nullptr, nullptr, 0}; // optional per-job trace (device buffers owned by the ctx)
@@ -294,6 +296,7 @@ struct Plan {
     unsigned grid;
     bool tmem;        // row-major only: staging tile in tensor memory (mk2_tmem.cuh)
     bool row64;       // Grain row-major: 512-clock tiles, 64 bytes per row and drain (mk2_grain_row64.cuh)
+    bool rowl2;       // ... with every warp's tile in L2-resident global scratch
 };
 
 Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
@@ -311,8 +314,13 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
     // picture (17% busy instead of the limiter) but its staging instructions cost what that returns
     // (9.9-10.1 Tb/s against 10.4 for the 256-clock shared-memory kernel, Grain section).
     p.row64 = rowmajor && ctx->cipher == 1 && ctx->row_staging == 2 && !ctx->block_user;
+    p.rowl2 = rowmajor && ctx->cipher == 1 && ctx->row_staging == 3;
     if (p.row64) {
         p.block = grain::row64::THREADS;
+        p.tg = grain::row64::NGRP;
+    }
+    if (p.rowl2) {
+        p.block = ctx->block_user ? ctx->block_user : BLOCK;
         p.tg = grain::row64::NGRP;
     }
     const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::WIN : 1u);
@@ -395,6 +403,21 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     const Plan p = make_plan(ctx, T, true, nchains);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
+    if (p.rowl2) {
+        if (!ctx->d_rowscratch)
+            CK(cudaMalloc(&ctx->d_rowscratch, (size_t)ctx->sm_count * (BLOCK / 32) * grain::row64::L2TILE_BYTES_PER_WARP));
+        if (ctx->row_lsb)
+            grain::row64::gen_rowmajor_l2_kernel<true><<<p.grid, p.block, 0, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base, aligned, ctx->d_rowscratch);
+        else
+            grain::row64::gen_rowmajor_l2_kernel<false><<<p.grid, p.block, 0, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->N, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base, aligned, ctx->d_rowscratch);
+        CK(cudaGetLastError());
+        ctx->last_launches++;
+        return MK2_OK;
+    }
     if (p.row64) {
         if (ctx->row_lsb)
             grain::row64::gen_rowmajor_kernel<true><<<p.grid, p.block, grain::row64::SMEM_BYTES, ctx->stream>>>(
@@ -715,6 +738,7 @@ int mk2_destroy(mk2_ctx *ctx)
     if (ctx->d_acc) cudaFree(ctx->d_acc);
     if (ctx->d_sum) cudaFree(ctx->d_sum);
     if (ctx->d_queue) cudaFree(ctx->d_queue);
+    if (ctx->d_rowscratch) cudaFree(ctx->d_rowscratch);
     if (ctx->trace.rec) cudaFree(ctx->trace.rec);
     if (ctx->trace.count) cudaFree(ctx->trace.count);
     if (ctx->d_slots) cudaFree(ctx->d_slots);
@@ -803,7 +827,8 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
 int mk2_set_row_staging(mk2_ctx *ctx, int mode)
 {
     if (!ctx) return MK2_E_ARG;
-    if (mode < 0 || mode > 2) return fail(ctx, MK2_E_ARG, "row staging mode must be 0 (automatic), 1 (shared memory) or 2 (tensor memory)");
+    if (mode < 0 || mode > 3)
+        return fail(ctx, MK2_E_ARG, "row staging mode must be 0 (automatic), 1 (shared memory), 2 (tensor memory) or 3 (L2 scratch)");
     ctx->row_staging = mode;
     return MK2_OK;
 }

@@ -45,6 +45,7 @@ constexpr int SMEM_BYTES = TILE_CLOCKS * SMEM_TS * 4 + (TILE_CLOCKS / 2) * 32 * 
 // warp and one shared-memory warp: a warp reaches the tensor-memory lanes of quadrant warp % 4 only) run the
 // same instructions and do not evict each other's loop from the instruction cache.
 struct Tile {
+    static constexpr int OUT_POLICY = 1;  // row stores ask L2 to keep the line (see store16)
     bool tm;         // tensor memory (else shared memory)
     uint32_t taddr;  // tensor memory: lane quadrant in bits 31:16, column 0
     uint32_t *col;   // shared memory: this thread's column
@@ -94,9 +95,51 @@ struct Tile {
     }
 };
 
+// The same tile in GLOBAL memory, sized and hinted to stay in L2 (mk2_set_row_staging(ctx, 3)): eight worker
+// warps per SM x 64 KiB = 74 MB of scratch for the whole GPU against 126 MB of L2.  A thread only ever reads
+// back the words it wrote itself (its own lane of [k][group][lane]), so there is nothing to synchronise: this
+// is a register spill area with a known address, written with one coalesced 128-byte store per warp and word
+// and read back the same way.  What it buys: no shared or tensor memory at all (eight warps, no STTM / LDTM,
+// no allocation barrier) and still 64 contiguous bytes per instance row and drain.  What it costs: the
+// keystream crosses the SM <-> L2 fabric three times (tile store, tile load, row store) instead of once.
+#ifndef MK2_L2TILE_ST_POLICY
+#define MK2_L2TILE_ST_POLICY 1   // tile stores: 0 = st.cg, 1 = L2 evict_last hint
+#endif
+#ifndef MK2_L2TILE_OUT_POLICY
+#define MK2_L2TILE_OUT_POLICY 2  // row stores: 0 = plain, 1 = L2 evict_last, 2 = L2 evict_first
+#endif
+struct L2Tile {
+    static constexpr int OUT_POLICY = MK2_L2TILE_OUT_POLICY;
+    uint32_t *col;   // this thread's lane of the warp's scratch slot
+    int ngrp;        // 8-clock groups per tile
+
+    __device__ __forceinline__ void store8(int grp, const uint32_t (&w)[8]) const
+    {
+        uint32_t *p = col + grp * 32;
+#if MK2_L2TILE_ST_POLICY == 1
+        unsigned long long pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p + k * ngrp * 32), "r"(w[k]), "l"(pol) : "memory");
+#else
+#pragma unroll
+        for (int k = 0; k < 8; ++k) __stcg(p + k * ngrp * 32, w[k]);
+#endif
+    }
+    __device__ __forceinline__ uint32_t load1(int idx) const { return __ldcg(col + idx * 32); }
+    __device__ __forceinline__ void load16(int first, uint32_t (&x)[16]) const
+    {
+        const uint32_t *p = col + first * 32;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = __ldcg(p + i * 32);
+    }
+    __device__ __forceinline__ void stores_done() const {}
+};
+
 // Eight keystream words of one 8-clock group -> bit transpose -> tile.  z[m] = keystream word of clock m.
-template <bool LSB>
-__device__ __forceinline__ void park_group(const Tile &tile, int grp, const uint32_t (&z)[8])
+template <bool LSB, class TT>
+__device__ __forceinline__ void park_group(const TT &tile, int grp, const uint32_t (&z)[8])
 {
     uint32_t w[8];
 #pragma unroll
@@ -108,7 +151,8 @@ __device__ __forceinline__ void park_group(const Tile &tile, int grp, const uint
 // Tile -> instance rows.  Whole tiles of complete, 16-byte aligned groups take the fast path: per k and per
 // sixteen groups, sixteen consecutive words -> four 4x4 byte transposes -> one 16-byte store to each of the
 // rows 8 q + k; the pieces of a row's 64-byte run follow one another within a few hundred cycles.
-__device__ __forceinline__ void drain(const Tile &tile, uint8_t *dst, uint64_t pitch, int ngrp, uint64_t nrows, bool aligned)
+template <class TT>
+__device__ __forceinline__ void drain(const TT &tile, uint8_t *dst, uint64_t pitch, int ngrp, uint64_t nrows, bool aligned)
 {
     tile.stores_done();
     if (aligned && ngrp == tile.ngrp && __all_sync(0xFFFFFFFFu, nrows == 32)) {
@@ -126,7 +170,7 @@ __device__ __forceinline__ void drain(const Tile &tile, uint8_t *dst, uint64_t p
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    store16<1>(dst + (uint64_t)(8 * q + k) * pitch + piece, make_uint4(y[0][q], y[1][q], y[2][q], y[3][q]));
+                    store16<TT::OUT_POLICY>(dst + (uint64_t)(8 * q + k) * pitch + piece, make_uint4(y[0][q], y[1][q], y[2][q], y[3][q]));
             }
         }
     } else {
@@ -146,8 +190,8 @@ __device__ __forceinline__ void drain(const Tile &tile, uint8_t *dst, uint64_t p
 // One worker warp: pop chains, run chunks of clocks, park keystream in `tile`, drain every 8 * tile.ngrp clocks.
 // Every thread of the warp runs along (the tensor-memory loads and stores are warp-collective): a thread whose
 // group does not exist (last, partial chain) works on the last real group and stores nothing.
-template <bool LSB>
-__device__ __forceinline__ void worker(const Tile &tile, const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
+template <bool LSB, class TT>
+__device__ __forceinline__ void worker(const TT &tile, const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
                                        unsigned long long *acc_out, uint8_t *out, uint64_t pitch, uint64_t N, uint64_t G, uint64_t T,
                                        uint32_t chunk, uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots,
                                        uint32_t mask, uint32_t *progress, uint32_t chain_base, bool aligned)
@@ -244,6 +288,23 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
     __syncthreads();
     tmem::fence_after_sync();
     if (warp == 0) tmem::dealloc(tmem_base_slot, 512u);
+}
+
+// Every worker warp with its tile in L2-resident scratch: scratch[(CTA * 8 + warp)][k][group][lane].
+constexpr size_t L2TILE_BYTES_PER_WARP = (size_t)TILE_CLOCKS * 32 * 4;
+template <bool LSB>
+__global__ void __launch_bounds__(BLOCK, 1)
+gen_rowmajor_l2_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out, unsigned long long *acc_out,
+                       uint8_t *__restrict__ out, uint64_t pitch, uint64_t N, uint64_t G, uint64_t T, uint32_t chunk,
+                       uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots, uint32_t mask, uint32_t *progress,
+                       uint32_t chain_base, bool aligned, uint32_t *scratch)
+{
+    L2Tile tile;
+    const uint32_t warp = threadIdx.x >> 5;
+    tile.col = scratch + ((size_t)blockIdx.x * (BLOCK / 32) + warp) * (L2TILE_BYTES_PER_WARP / 4) + (threadIdx.x & 31u);
+    tile.ngrp = NGRP;
+    worker<LSB>(tile, state, acc, state_out, acc_out, out, pitch, N, G, T, chunk, chunks_per_chain, q, slots, mask, progress,
+                chain_base, aligned);
 }
 
 }  // namespace row64

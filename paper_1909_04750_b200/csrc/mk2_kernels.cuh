@@ -792,6 +792,13 @@ __device__ __forceinline__ void store16(uint8_t *p, uint4 v)
         asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                      "r"(v.w), "l"(pol)
                      : "memory");
+    } else if constexpr (POLICY == 2) {
+        // streaming: the row piece is complete when it is written, L2 may write it back first
+        unsigned long long pol;
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                     "r"(v.w), "l"(pol)
+                     : "memory");
     } else {
         *reinterpret_cast<uint4 *>(p) = v;
     }

@@ -90,7 +90,8 @@ class MickeyGenerator:
         self._ck(self._lib.mk2_set_chunk_clocks(self._ctx, int(clocks)), "mk2_set_chunk_clocks")
 
     def set_row_staging(self, mode: int):
-        """Tuning knob: row-major staging tile in shared memory (1) or tensor memory (2); 0 = automatic."""
+        """Tuning knob: row-major staging tile in shared memory (1), tensor memory (2) or (Grain only) L2-resident
+        global scratch (3); 0 = automatic."""
         self._knobs_touched = True
         self._ck(self._lib.mk2_set_row_staging(self._ctx, int(mode)), "mk2_set_row_staging")
 

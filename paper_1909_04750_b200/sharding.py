@@ -56,7 +56,7 @@ def allreduce_checksum(local_sum: int, device=None, group=None) -> int:
     import torch
     import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return from_i64(to_i64(local_sum))
     t = torch.tensor([to_i64(local_sum)], dtype=torch.int64, device=device or "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)  # two's-complement wrap == mod 2^64

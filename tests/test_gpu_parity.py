@@ -885,11 +885,13 @@ def test_grain_bulk_vs_oracle(pkg, oracle, block, chunk, torch_cuda):
     assert np.array_equal(dev.cpu().numpy(), oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb"))
 
 
+@pytest.mark.parametrize("staging", [2, 3])
 @pytest.mark.parametrize("N,T,chunk", [(32 * 70 + 11, 1000, 0), (1 << 15, 4096 + 520, 1024), (64, 8, 0), (4099, 136, 0)])
-def test_grain_rowmajor_512_clock_tiles(pkg, oracle, N, T, chunk, torch_cuda):
-    """The opt-in Grain row-major kernel with 512-clock tiles split between tensor and shared memory
-    (mk2_set_row_staging(ctx, 2); csrc/mk2_grain_row64.cuh): whole tiles, short tails, partial last groups,
-    both byte orders, unaligned rows -- same bytes as the oracle and as the default kernel."""
+def test_grain_rowmajor_512_clock_tiles(pkg, oracle, N, T, chunk, staging, torch_cuda):
+    """The opt-in Grain row-major kernels with 512-clock tiles (csrc/mk2_grain_row64.cuh): split between tensor
+    and shared memory (mk2_set_row_staging(ctx, 2)) or in L2-resident global scratch (3): whole tiles, short
+    tails, partial last groups, both byte orders, unaligned rows -- same bytes as the oracle and as the default
+    kernel."""
     from paper_1909_04750_b200 import grain
 
     rng = np.random.default_rng(N + T)
@@ -897,7 +899,7 @@ def test_grain_rowmajor_512_clock_tiles(pkg, oracle, N, T, chunk, torch_cuda):
     ivs = rng.integers(0, 256, (N, 8), dtype=np.uint8)
     want = oracle.grain_bulk_rowmajor(keys, ivs, T)
     with grain.GrainGenerator(0) as gen:
-        gen.set_row_staging(2)
+        gen.set_row_staging(staging)
         gen.set_chunk_clocks(chunk)
         row = gen.init_material(keys, ivs).generate_rowmajor(T)
         csum = gen.checksum()
