@@ -417,9 +417,25 @@ def measure_workload(env: Env, name: str, n: int, clocks: int, layout: str, firs
     launches = 0
     plan = None
 
+    # c5 is the reference's one-shot call (mickey_sliced_words restarts from the key/IV load on every call,
+    # kernels.py:189-200): mk2_bulk_rowmajor with everything on the device = ONE fused kernel (csrc/mk2_fused.cuh)
+    one_shot = explicit and out_mode == "full"
+
+    one_shot_sum = 0
+
     def step(i: int, record: bool):
-        nonlocal launches, plan
+        nonlocal launches, plan, one_shot_sum
         e0, e1 = env.event(), env.event()
+        if one_shot:
+            e0.record(stream)
+            _, one_shot_sum = gen.bulk_rowmajor(d_keys, d_ivs, 80, clocks, out)
+            e1.record(stream)
+            launches += gen.last_kernel_launches
+            if record:
+                gen_events.append((e0, e1, clocks))
+            if plan is None:
+                plan = gen.last_plan()
+            return
         e0.record(stream)
         if explicit:
             gen.init_material(d_keys, d_ivs, 80)
@@ -469,7 +485,24 @@ def measure_workload(env: Env, name: str, n: int, clocks: int, layout: str, firs
     init_ms = [e0.elapsed_time(e1) for e0, e1 in init_events]
     gen_clk = sum(tc for _, _, tc in gen_events)
     kernel_ms_total = sum(gen_ms)
-    checksum = gen.checksum()                          # of the last step's keystream, this rank's range
+    checksum = one_shot_sum if one_shot else gen.checksum()   # of the last step's keystream, this rank's range
+    two_call = None
+    if one_shot:                                       # the same batch as pack + init + keystream kernels, for the split
+        ti, tg = [], []
+        for _ in range(3):
+            ev = [env.event() for _ in range(3)]
+            ev[0].record(stream)
+            gen.init_material(d_keys, d_ivs, 80)
+            ev[1].record(stream)
+            gen.generate_rowmajor(clocks, out)
+            ev[2].record(stream)
+            env.torch.cuda.synchronize()
+            ti.append(ev[0].elapsed_time(ev[1]))
+            tg.append(ev[1].elapsed_time(ev[2]))
+        assert gen.checksum() == checksum, "one-shot and two-call checksums differ"
+        two_call = {"init_ms": min(ti), "keystream_ms": min(tg), "ms_per_step": min(a + b for a, b in zip(ti, tg)),
+                    "note": "mk2_init_from_material + mk2_generate_rowmajor (pack_uniform_kernel, init_kernel, "
+                            "tmem::gen_rowmajor_kernel): input words and state pass through HBM; same checksum"}
 
     # ---- roofline of the dominant kernel (keystream loop), this rank.
     # Algorithmic LOP3 per clock of the kernel as built: the clock runs in blocks of K clocks with R's reduction
@@ -480,9 +513,14 @@ def measure_workload(env: Env, name: str, n: int, clocks: int, layout: str, firs
     rblock, per_block = lib.mk2_rblock(which), lib.mk2_lop3_per_block(which)
     lop3_per_clock = per_block / rblock
     lop3_peak = env.peak()
+    irb, ipb = lib.mk2_rblock(2), lib.mk2_lop3_per_block(2)
     lane_ops = n * gen_clk * lop3_per_clock / 32          # algorithmic LOP3 lane-ops in the timed launches
+    if one_shot:                                          # the launch also runs the 160 load clocks + 100 pre-clocks
+        lane_ops += n / 32 * (160 + 100) * ipb / irb * len(gen_events)
     achieved = lane_ops / (kernel_ms_total * 1e-3)
     achieved_survey = achieved * LOP3_PER_CLOCK_SURVEY / lop3_per_clock
+    if one_shot:  # 329 per load clock, 327 per pre-clock and keystream clock
+        achieved_survey = n / 32 * (160 * 329 + (100 + clocks) * 327) * len(gen_events) / (kernel_ms_total * 1e-3)
     hbm_gbs = (n * gen_clk / 8) / (kernel_ms_total * 1e-3) / 1e9
     launch_clocks = gen_events[0][2] if gen_events else 0
     # in-run traffic model of one launch: the stores of the keystream itself plus the state parking of the
@@ -491,10 +529,16 @@ def measure_workload(env: Env, name: str, n: int, clocks: int, layout: str, firs
     block_threads, chunk = plan if plan else (0, 0)
     jobs = ((n + 1023) // 1024) * (-(-launch_clocks // chunk) if chunk else 0)
     traffic_model = n * launch_clocks // 8 + jobs * 32 * 2 * (800 + 8)
+    alg_bytes = n * launch_clocks // 8
+    if one_shot:                                          # rows out + key/IV records in; nothing else touches HBM
+        jobs = (n + 1023) // 1024
+        traffic_model = alg_bytes = n * launch_clocks // 8 + n * 20
     ncu_bytes, ncu_src = NCU_TRAFFIC.get((layout, n, launch_clocks), (None, None))
     peaks = env.peaks
     roofline = {
-        "bound": "lop3", "kernel": "gen_colmajor_kernel" if layout == "colmajor" else "tmem::gen_rowmajor_kernel",
+        "bound": "lop3", "kernel": ("gen_colmajor_kernel" if layout == "colmajor" else
+                                    "fused::bulk_rowmajor_kernel (key/IV records -> input words -> load clocks -> "
+                                    "pre-clocks -> keystream -> rows)" if one_shot else "tmem::gen_rowmajor_kernel"),
         "achieved": achieved / 1e12, "peak": lop3_peak / 1e12, "unit": "Tlane-op/s", "frac": achieved / lop3_peak,
         "peak_source": "measured live by mk2_lop3_peak (dependency-free LOP3 kernel) on this GPU",
         "algorithmic_ops_per_launch": lane_ops / max(1, len(gen_events)),
@@ -510,18 +554,25 @@ def measure_workload(env: Env, name: str, n: int, clocks: int, layout: str, firs
         "traffic_source": (f"{ncu_src}: ncu --set full capture of a launch of exactly this geometry, committed earlier; "
                            f"NOT measured in this run") if ncu_src else None,
         "traffic_model": traffic_model,
-        "traffic_model_source": "computed in this run from the launch plan: keystream stores + state parking of every "
+        "traffic_model_source": ("computed in this run: keystream rows out + key/IV records in (input words and state "
+                                 "stay on the SM)") if one_shot else
+                                "computed in this run from the launch plan: keystream stores + state parking of every "
                                 "chain-chunk job (2 x 808 B per thread)",
-        "algorithmic_bytes_per_launch": n * launch_clocks // 8,
+        "algorithmic_bytes_per_launch": alg_bytes,
         "hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": hbm_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                 "peak_source": f"MEASURED_PEAKS.json ({env.peaks_src})", "note": "0.125 B stored per keystream bit; not binding"},
     }
     # whole step (pack + key/IV load + pre-clocks + keystream) against the same LOP3 peak: 160 load clocks and
     # 100 pre-clocks per instance at the init kernel's block count, T keystream clocks at the keystream kernel's
-    irb, ipb = lib.mk2_rblock(2), lib.mk2_lop3_per_block(2)
     step_ops = n / 32 * ((160 + 100) * ipb / irb + clocks * lop3_per_clock) * steps
     split = {
+        "one_shot": True, "ms_per_step": kernel_ms_total / max(1, steps),
+        "note": "one fused kernel per step: key/IV records -> input words (tensor memory) -> 160 load clocks -> 100 "
+                "pre-clocks -> keystream -> rows; roofline.frac counts the load and pre-clocks' LOP3 too",
+        "whole_step_lop3_frac": step_ops / (local_ms * 1e-3) / lop3_peak,
+        "two_call_path": two_call,
+    } if one_shot else {
         "init_ms_per_step": sum(init_ms) / max(1, steps), "keystream_ms_per_step": kernel_ms_total / max(1, steps),
         "init_note": ("pack_uniform_kernel (u8[N][10] key / IV rows -> bitsliced input words) + init_kernel" if explicit
                       else "pack_counter_kernel + init_kernel") + ": 160 load clocks + 100 pre-clocks per instance",
@@ -917,9 +968,9 @@ def traffic_child(args):
                else torch.empty((n, clocks // 8), dtype=torch.uint8, device=dev))
         for _ in range(2):
             if args.workload == "c5":
-                gen.init_material(d_keys, d_ivs, 80)
-            else:
-                gen.init_counter(KEY, 0, n)
+                gen.bulk_rowmajor(d_keys, d_ivs, 80, clocks, out)
+                continue
+            gen.init_counter(KEY, 0, n)
             gen.generate_colmajor(clocks, out) if layout == "colmajor" else gen.generate_rowmajor(clocks, out)
         torch.cuda.synchronize()
 
@@ -937,7 +988,7 @@ def measure_traffic_live(workload: str, timeout_s: float = 300.0):
     if not Path(ncu).exists():
         return None, "ncu not found"
     layout = WORKLOADS[workload][2]
-    kern = "gen_colmajor_kernel" if layout == "colmajor" else "gen_rowmajor_kernel"
+    kern = "gen_colmajor_kernel" if layout == "colmajor" else "bulk_rowmajor_kernel" if workload == "c5" else "gen_rowmajor_kernel"
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--print-units", "base",
            "--csv", "-k", f"regex:{kern}", "--launch-skip", "1", "--launch-count", "1",
            sys.executable, str(Path(__file__).resolve()), "--traffic-child", "--workload", workload]

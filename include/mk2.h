@@ -252,6 +252,13 @@ int mk2_host_free(void *p);
  * measured: it does not stay, 7.2 Tb/s against 10.4 -- kept as a documented
  * negative result).  Mode 3 on a MICKEY context behaves like 0. */
 int mk2_set_row_staging(mk2_ctx *ctx, int mode);
+/* Tuning knob: mk2_bulk_rowmajor with key/IV arrays AND output on the device runs
+ * as one kernel (csrc/mk2_fused.cuh: records -> input words in tensor memory ->
+ * load clocks -> pre-clocks -> keystream -> rows; neither the bitsliced material
+ * nor the state passes through HBM) when the IV length is a whole number of bytes,
+ * IV records are 10 bytes apart and both arrays are 16-byte aligned.  enable = 0
+ * forces the pack / init / keystream kernels of the block pipeline (A/B, tests). */
+int mk2_set_bulk_fused(mk2_ctx *ctx, int enable);
 int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 
 /* Diagnostics: per-job trace of the column-major persistent kernel.  Records

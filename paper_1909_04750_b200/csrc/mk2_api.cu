@@ -18,6 +18,7 @@
 #include "mk2_tmem.cuh"
 #include "mk2_grain.cuh"
 #include "mk2_grain_row64.cuh"
+#include "mk2_fused.cuh"
 #include "mk2_seedgen.cuh"
 #include "mk2_host_lanes.h"
 
@@ -83,6 +84,7 @@ struct mk2_ctx {
     int row_staging = 0;                 // row-major staging tile: 0 = automatic, 1 = shared memory, 2 = tensor memory,
                                          // 3 = L2-resident scratch (Grain only)
     uint32_t *d_rowscratch = nullptr;    // staging mode 3: one 64 KiB tile per worker warp (lazy)
+    int bulk_fused = 1;                  // mk2_bulk_rowmajor with device buffers: 1 = the one-kernel path when eligible
     int last_plan_block = 0;
     uint32_t last_plan_chunk = 0;
     Trace trace = {nullptr, nullptr, 0}; // optional per-job trace (device buffers owned by the ctx)
@@ -833,6 +835,13 @@ int mk2_set_row_staging(mk2_ctx *ctx, int mode)
     return MK2_OK;
 }
 
+int mk2_set_bulk_fused(mk2_ctx *ctx, int enable)
+{
+    if (!ctx) return MK2_E_ARG;
+    ctx->bulk_fused = enable ? 1 : 0;
+    return MK2_OK;
+}
+
 int mk2_set_stage_bytes(mk2_ctx *ctx, uint64_t bytes)
 {
     if (!ctx) return MK2_E_ARG;
@@ -1369,6 +1378,57 @@ static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *
     const bool in_dev = is_device_ptr(keys), out_dev = out_mem == Mem::Device;
     if (iv_bits && is_device_ptr(ivs) != in_dev) return fail(ctx, MK2_E_ARG, "keys and ivs must both be host or both be device pointers");
     const uint64_t block_inst = 2ull * 8ull * (uint64_t)ctx->sm_count * 1024ull;  // two chains per worker warp
+    // Everything on the device already: ONE kernel for the whole batch (mk2_fused.cuh) -- input words and state
+    // never leave the SM.  It wants whole IV bytes, 10-byte IV records and 16-byte aligned arrays (what the
+    // 128-bit record loads need); anything else takes the block pipeline below.
+    if (in_dev && out_dev && ctx->bulk_fused && ctx->row_staging != 1 && iv_bits % 8 == 0 &&
+        reinterpret_cast<uintptr_t>(keys) % 16 == 0 &&
+        (iv_bits == 0 || (iv_stride == 10 && reinterpret_cast<uintptr_t>(ivs) % 16 == 0))) {
+        const bool resume = N <= block_inst;  // as below: a single block leaves a state to resume from
+        const uint64_t G = (N + 31) / 32;
+        ctx->ready = false;
+        if (resume) {
+            if ((rc = init_common(ctx, N))) return rc;
+        } else {
+            ctx->N = ctx->G = 0;
+        }
+        ctx->last_launches = 0;
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        CK(cudaMemsetAsync(ctx->d_sum, 0, sizeof(unsigned long long), ctx->stream));
+        CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(SchedQueue), ctx->stream));
+        const uint64_t jobs = ((G + 31) / 32 + BLOCK / 32 - 1) / (BLOCK / 32);
+        const uint64_t sms = ctx->max_grid ? std::min<uint64_t>(ctx->max_grid, (uint64_t)ctx->sm_count) : (uint64_t)ctx->sm_count;
+        // whole rounds as eight-chain jobs; a last round that would occupy at most half of the SMs as four-chain jobs
+        const uint64_t rem = jobs % sms;
+        const unsigned long long full_jobs = rem && 2 * rem <= sms ? jobs - rem : jobs;
+        const unsigned grid = (unsigned)std::min<uint64_t>(sms, full_jobs + 2 * (jobs - full_jobs));
+        uint32_t *st = resume ? ctx->d_state : nullptr;
+        unsigned long long *ac = resume ? ctx->d_acc : nullptr;
+        const bool aligned = reinterpret_cast<uintptr_t>(out) % 16 == 0 && pitch_bytes % 16 == 0;
+        if (aligned)
+            fused::bulk_rowmajor_kernel<true><<<grid, BLOCK, 0, ctx->stream>>>(keys, ivs, (int)iv_bits / 8, N, G, T,
+                static_cast<uint8_t *>(out), pitch_bytes, &ctx->d_queue->head, full_jobs, ctx->d_sum, ctx->g_offset, st, ac);
+        else
+            fused::bulk_rowmajor_kernel<false><<<grid, BLOCK, 0, ctx->stream>>>(keys, ivs, (int)iv_bits / 8, N, G, T,
+                static_cast<uint8_t *>(out), pitch_bytes, &ctx->d_queue->head, full_jobs, ctx->d_sum, ctx->g_offset, st, ac);
+        CK(cudaGetLastError());
+        unsigned long long v = 0;
+        CK(cudaMemcpyAsync(&v, ctx->d_sum, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+        ctx->timing_open = false;
+        ctx->last_launches = 1;
+        ctx->last_plan_block = BLOCK;
+        ctx->last_plan_chunk = (uint32_t)std::min<uint64_t>(T, 0x7FFFFF00ull);
+        if (checksum) *checksum = v;
+        if (resume) {
+            ctx->clocks = T;
+            ctx->cipher = 0;
+            ctx->ready = true;
+        }
+        return MK2_OK;
+    }
     if (!ctx->h2d) {
         CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {

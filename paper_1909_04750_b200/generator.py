@@ -95,6 +95,11 @@ class MickeyGenerator:
         self._knobs_touched = True
         self._ck(self._lib.mk2_set_row_staging(self._ctx, int(mode)), "mk2_set_row_staging")
 
+    def set_bulk_fused(self, enable: bool):
+        """Tuning knob: device-to-device bulk_rowmajor as one fused kernel (default) or as pack / init / keystream."""
+        self._knobs_touched = True
+        self._ck(self._lib.mk2_set_bulk_fused(self._ctx, int(bool(enable))), "mk2_set_bulk_fused")
+
     def set_stage_bytes(self, nbytes: int):
         """Tuning knob: bytes per device staging tile when the output buffer is in host memory."""
         self._knobs_touched = True

@@ -471,6 +471,12 @@ def test_full_coverage_checksum_c5_explicit_material(pkg, oracle, torch_cuda):
         assert int(col.view("<u8").sum(dtype=np.uint64)) == want
         rows, csum = gen.bulk_rowmajor(keys, ivs, 80, T)
         assert csum == want
+        # the same batch resident on the device: the one-kernel path (csrc/mk2_fused.cuh), every pair
+        dk, di = torch_cuda.from_numpy(keys).cuda(), torch_cuda.from_numpy(ivs).cuda()
+        drows = torch_cuda.empty((N, T // 8), dtype=torch_cuda.uint8, device="cuda")
+        _, dsum = gen.bulk_rowmajor(dk, di, 80, T, drows)
+        assert gen.last_kernel_launches == 1 and dsum == want
+        assert np.array_equal(drows.cpu().numpy(), rows)
         bits = np.unpackbits(rows[4096:4160], axis=1)              # rows -> column words of one 64-lane batch
         words = (bits.T.astype(np.uint64) << np.arange(64, dtype=np.uint64)).sum(axis=1, dtype=np.uint64)
         assert np.array_equal(words, col[:, 128:130].copy().view("<u8").reshape(-1))
@@ -570,8 +576,9 @@ def test_c3_full_size_rowmajor(pkg, golden, oracle, torch_cuda):
 
 def test_c5_full_size_fresh_material(pkg, oracle, torch_cuda):
     """BASELINE config 5 at its FULL size -- 2^26 fresh (key, IV) pairs x 1 Kbit, explicit material arrays on the
-    device, 8.6 GB of row-major keystream: init + generate and the one-shot bulk call (28 pipeline blocks) agree on
-    every byte and on the checksum; sampled rows bit-exact vs the oracle."""
+    device, 8.6 GB of row-major keystream: init + generate, the one-shot bulk call as ONE fused kernel
+    (csrc/mk2_fused.cuh) and the same call as 28 pipeline blocks of pack / init / keystream kernels agree on every
+    byte and on the checksum; sampled rows bit-exact vs the oracle."""
     torch = torch_cuda
     N, T = 1 << 26, 1024
     if _free_gib(torch) < 2 * N * T / 8 / 2**30 + 12:
@@ -593,7 +600,12 @@ def test_c5_full_size_fresh_material(pkg, oracle, torch_cuda):
         rows2 = torch.empty_like(rows)
         _, csum2 = gen.bulk_rowmajor(keys, ivs, 80, T, rows2)
         torch.cuda.synchronize()
-        assert csum2 == csum and torch.equal(rows, rows2)
+        assert gen.last_kernel_launches == 1 and csum2 == csum and torch.equal(rows, rows2)
+        rows2.zero_()
+        gen.set_bulk_fused(False)
+        _, csum3 = gen.bulk_rowmajor(keys, ivs, 80, T, rows2)
+        torch.cuda.synchronize()
+        assert gen.last_kernel_launches > 28 and csum3 == csum and torch.equal(rows, rows2)
         gen.set_stream(None)
     del rows, rows2, keys, ivs
     torch.cuda.empty_cache()
@@ -1040,6 +1052,46 @@ def test_rowmajor_tensor_memory_staging(pkg, oracle, N, T, block, chunk):
         assert gen.checksum() == c_tmem
     assert np.array_equal(got, want)
     assert np.array_equal(a[:, : T // 8], want)
+
+
+@pytest.mark.parametrize("N,T,iv_bits,pad", [(1024, 1024, 80, 0), (32 * 70 + 11, 1000, 80, 0), (5, 8, 0, 0), (4099, 264, 32, 3),
+                                             (1 << 15, 4096 + 520, 80, 0), (2 * 8 * 148 * 1024 + 4096 + 7, 128, 16, 0),
+                                             (1 << 16, 256, 0, 16)])
+def test_bulk_rowmajor_fused_kernel(pkg, oracle, N, T, iv_bits, pad, torch_cuda):
+    """mk2_bulk_rowmajor with key/IV arrays and output on the device = ONE kernel (csrc/mk2_fused.cuh: records ->
+    input words in tensor memory -> load clocks -> pre-clocks -> keystream -> rows): the same bytes and checksum
+    as the pack / init / keystream kernels (mk2_set_bulk_fused(0)) and as the oracle; partial last group and
+    chain, IV lengths 0 / 16 / 32 / 80 bits, short tails, unaligned rows, more than one pipeline block, and the
+    state it leaves for a resuming call (mickey_sliced_words + words_lane_major_bytes, kernels.py:189-200, :615-621)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(N + T)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    dk, di = torch.from_numpy(keys).cuda(), torch.from_numpy(ivs).cuda()
+    sample = np.unique(np.concatenate([np.arange(min(N, 96)), np.arange(max(0, N - 96), N), rng.integers(0, N, 64)]))
+    want = oracle.bulk_rowmajor(keys[sample], ivs[sample], iv_bits, T)
+    resumable = N <= 2 * 8 * torch.cuda.get_device_properties(0).multi_processor_count * 1024
+    with pkg.MickeyGenerator(0) as gen:
+        a = torch.zeros((N, T // 8 + pad), dtype=torch.uint8, device="cuda")
+        _, ca = gen.bulk_rowmajor(dk, di, iv_bits, T, a)
+        assert gen.last_kernel_launches == 1                       # the fused path ran
+        if resumable:
+            more = gen.generate_rowmajor(64)
+            resumed = gen.checksum()
+        else:
+            with pytest.raises(pkg.Mk2Error):
+                gen.generate_rowmajor(8)
+        gen.set_bulk_fused(False)
+        b = torch.zeros((N, T // 8 + pad), dtype=torch.uint8, device="cuda")
+        _, cb = gen.bulk_rowmajor(dk, di, iv_bits, T, b)
+        assert gen.last_kernel_launches > 1
+        if resumable:
+            assert np.array_equal(more, gen.generate_rowmajor(64)) and resumed == gen.checksum()
+    torch.cuda.synchronize()
+    assert ca == cb and bool((a == b).all().item())
+    assert np.array_equal(a.cpu().numpy()[sample][:, : T // 8], want)
+    if pad:
+        assert not bool(a[:, T // 8:].any().item())
 
 
 def test_bulk_rowmajor_one_shot_pipelined_blocks(pkg, oracle, torch_cuda):
