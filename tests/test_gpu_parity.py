@@ -1054,6 +1054,16 @@ def test_rowmajor_tensor_memory_staging(pkg, oracle, N, T, block, chunk):
     assert np.array_equal(a[:, : T // 8], want)
 
 
+def test_c_abi_from_plain_c(c_abi_consumer):
+    """The drop-in boundary used from plain C (tests/c/abi_consumer.c: include/mk2.h + libmk2.so, malloc'ed host
+    buffers): the eSTREAM vector on 70 instances through init + generate and through the one-shot bulk call."""
+    import subprocess
+
+    res = subprocess.run([str(c_abi_consumer)], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, (res.returncode, res.stdout, res.stderr)
+    assert res.stdout.startswith("ok: 70 instances x 128 bits")
+
+
 @pytest.mark.parametrize("N,T,iv_bits,pad", [(1024, 1024, 80, 0), (32 * 70 + 11, 1000, 80, 0), (5, 8, 0, 0), (4099, 264, 32, 3),
                                              (1 << 15, 4096 + 520, 80, 0), (2 * 8 * 148 * 1024 + 4096 + 7, 128, 16, 0),
                                              (1 << 16, 256, 0, 16)])

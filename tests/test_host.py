@@ -37,6 +37,20 @@ def test_no_cpu_fallback_without_device():
         pkg.mickey_sliced_words([MickeyKeyIv(bytes(10), b"")], 8)
 
 
+def test_c_abi_from_plain_c_fails_loudly_without_device(c_abi_consumer):
+    """A C program that includes only include/mk2.h links against libmk2.so; without an sm_100 device mk2_create
+    returns MK2_E_NODEVICE with a message (exit code 3 of tests/c/abi_consumer.c) -- no crash, no CPU path."""
+    import subprocess
+
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by test_c_abi_from_plain_c in the GPU suite")
+    res = subprocess.run([str(c_abi_consumer)], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 3, (res.returncode, res.stdout, res.stderr)
+    assert "no CPU fallback" in res.stderr
+
+
 def test_product_package_never_imports_oracle():
     for path in (ROOT / "paper_1909_04750_b200").rglob("*.py"):
         text = path.read_text()
