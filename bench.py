@@ -929,22 +929,32 @@ def small_call_latency(env: Env) -> dict:
     unpooled = best(fresh, 8)
     keys, ivs, nbits, _ = pkg.mickey.pack_materials(mats, 64)
     pack_us = best(lambda: pkg.mickey.pack_materials(mats, 64), 10)[0]
-    with pkg.MickeyGenerator(env.local) as g:
-        g.init_material(keys, ivs, 32).generate_colmajor(4096)
-        kern, wall = [], []
-        for _ in range(20):
-            t0 = time.perf_counter()
-            g.init_material(keys, ivs, 32)
-            k = g.last_kernel_ms
-            g.generate_colmajor(4096)
-            k += g.last_kernel_ms
-            wall.append(time.perf_counter() - t0)
-            kern.append(k)
+    def abi_calls(small_batch: bool):
+        with pkg.MickeyGenerator(env.local) as g:
+            g.set_small_batch(small_batch)
+            g.init_material(keys, ivs, 32).generate_colmajor(4096)
+            kern, wall = [], []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                g.init_material(keys, ivs, 32)
+                k = g.last_kernel_ms
+                g.generate_colmajor(4096)
+                k += g.last_kernel_ms
+                wall.append(time.perf_counter() - t0)
+                kern.append(k)
+        return kern, wall
+
+    kern, wall = abi_calls(True)
+    kern_tpg, _ = abi_calls(False)
     return {"call": "mickey_sliced_words(64 lanes, 4096 clocks) -> uint64[4096] on the host",
             "idle_context_reused_us": {"best": pooled[0], "median": pooled[1]},
             "new_context_per_call_us": {"best": unpooled[0], "median": unpooled[1]},
             "python_validation_and_packing_us": pack_us,
             "c_abi_init_plus_generate_us": {"wall_best": min(wall) * 1e6, "device_kernels_best": min(kern) * 1e3},
+            "kernels": "warp-per-group small-batch kernels (csrc/mk2_coop.cuh): the 200 state bits of a 32-instance group "
+                       "spread over the lanes of one warp",
+            "device_kernels_thread_per_group_us": min(kern_tpg) * 1e3,
+            "small_batch_speedup_on_device": min(kern_tpg) / min(kern),
             "overhead_over_kernel_time_us": pooled[0] - min(kern) * 1e3,
             "overhead_over_kernel_time_excluding_python_packing_us": pooled[0] - min(kern) * 1e3 - pack_us}
 

@@ -259,6 +259,13 @@ int mk2_set_row_staging(mk2_ctx *ctx, int mode);
  * IV records are 10 bytes apart and both arrays are 16-byte aligned.  enable = 0
  * forces the pack / init / keystream kernels of the block pipeline (A/B, tests). */
 int mk2_set_bulk_fused(mk2_ctx *ctx, int enable);
+/* Tuning knob: small batches (up to 2048 groups = 65536 instances; the reference's
+ * own calling unit is 64 lanes, kernels.py:189-200, cli.py:219-231) are initialised
+ * and clocked column-major by warp-per-group kernels (csrc/mk2_coop.cuh: the 200
+ * state bits of a group spread over the lanes of a warp, neighbours and taps by
+ * shuffle), which cut the latency of a call several times.  enable = 0 forces the
+ * thread-per-group throughput kernels (A/B, tests).  Same state layout either way. */
+int mk2_set_small_batch(mk2_ctx *ctx, int enable);
 int mk2_last_plan(const mk2_ctx *ctx, int *block_threads, uint32_t *chunk_clocks);
 
 /* Diagnostics: per-job trace of the column-major persistent kernel.  Records

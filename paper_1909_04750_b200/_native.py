@@ -36,6 +36,7 @@ SYMBOLS = {
     "mk2_bulk_rowmajor": (C.c_int, [_vp, _vp, _vp, C.c_uint32, C.c_uint32, _u64, _u64, _vp, _u64, C.POINTER(_u64)]),
     "mk2_set_row_staging": (C.c_int, [_vp, C.c_int]),
     "mk2_set_bulk_fused": (C.c_int, [_vp, C.c_int]),
+    "mk2_set_small_batch": (C.c_int, [_vp, C.c_int]),
     "mk2_last_plan": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_uint32)]),
     "mk2_sync": (C.c_int, [_vp]),
     "mk2_trim": (C.c_int, [_vp]),

@@ -95,6 +95,11 @@ class MickeyGenerator:
         self._knobs_touched = True
         self._ck(self._lib.mk2_set_row_staging(self._ctx, int(mode)), "mk2_set_row_staging")
 
+    def set_small_batch(self, enable: bool):
+        """Tuning knob: warp-per-group kernels for small batches (default) or the throughput kernels at every size."""
+        self._knobs_touched = True
+        self._ck(self._lib.mk2_set_small_batch(self._ctx, int(bool(enable))), "mk2_set_small_batch")
+
     def set_bulk_fused(self, enable: bool):
         """Tuning knob: device-to-device bulk_rowmajor as one fused kernel (default) or as pack / init / keystream."""
         self._knobs_touched = True

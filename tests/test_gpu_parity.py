@@ -1054,6 +1054,34 @@ def test_rowmajor_tensor_memory_staging(pkg, oracle, N, T, block, chunk):
     assert np.array_equal(a[:, : T // 8], want)
 
 
+@pytest.mark.parametrize("N,T,iv_bits", [(1, 8, 0), (32, 1000, 32), (64, 4096 + 37, 80), (1000, 333, 13), (5000, 2048, 80),
+                                         (65536, 96, 80)])
+def test_small_batch_warp_per_group_kernels(pkg, oracle, N, T, iv_bits):
+    """Small batches (up to 2048 groups; the reference's own unit is 64 lanes, kernels.py:189-200) are initialised
+    and clocked by warp-per-group kernels (csrc/mk2_coop.cuh: state spread over the lanes, taps and neighbours by
+    shuffle).  Same words, state and checksum as the thread-per-group kernels (mk2_set_small_batch(0)) and as the
+    oracle; a context initialised by one kind and clocked, resumed or exported by the other agrees too."""
+    rng = np.random.default_rng(N * 7 + T)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    want = oracle.bulk_colmajor(keys, ivs, iv_bits, T + 40)
+    with pkg.MickeyGenerator(0) as a, pkg.MickeyGenerator(0) as b:
+        b.set_small_batch(False)
+        wa = a.init_material(keys, ivs, iv_bits).generate_colmajor(T)
+        wb = b.init_material(keys, ivs, iv_bits).generate_colmajor(T)
+        assert a.last_plan()[0] == 128 and np.array_equal(wa, wb) and np.array_equal(wa, want[:T])
+        assert a.checksum() == b.checksum() and np.array_equal(a.export_state(), b.export_state())
+        # cross over: the state the warp-per-group kernels left is continued by the throughput kernels and back
+        a.set_small_batch(False)
+        b.set_small_batch(True)
+        ma, mb = a.generate_colmajor(40), b.generate_colmajor(40)
+        assert np.array_equal(ma, want[T:]) and np.array_equal(mb, want[T:]) and a.checksum() == b.checksum()
+        # row-major output of a state initialised by the small-batch init kernel
+        b.init_material(keys, ivs, iv_bits)
+        if T % 8 == 0:
+            assert np.array_equal(b.generate_rowmajor(T), oracle.bulk_rowmajor(keys, ivs, iv_bits, T))
+
+
 def test_c_abi_from_plain_c(c_abi_consumer):
     """The drop-in boundary used from plain C (tests/c/abi_consumer.c: include/mk2.h + libmk2.so, malloc'ed host
     buffers): the eSTREAM vector on 70 instances through init + generate and through the one-shot bulk call."""
