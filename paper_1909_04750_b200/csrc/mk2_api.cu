@@ -420,6 +420,19 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
 // instance of chain_base.
 int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t chain_base, uint64_t nchains)
 {
+    if (ctx->cipher == 0 && ctx->small_batch && ctx->G <= COOP_MAX_GROUPS && chain_base == 0 && nchains == (ctx->G + 31) / 32) {
+        if (ctx->row_lsb)
+            coop::gen_rowmajor_kernel<true><<<coop_grid(ctx), 32 * coop::WARPS, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, pitch,
+                                                                                               ctx->N, ctx->G, T);
+        else
+            coop::gen_rowmajor_kernel<false><<<coop_grid(ctx), 32 * coop::WARPS, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, out, pitch,
+                                                                                                ctx->N, ctx->G, T);
+        CK(cudaGetLastError());
+        ctx->last_launches++;
+        ctx->last_plan_block = 32 * coop::WARPS;
+        ctx->last_plan_chunk = (uint32_t)std::min<uint64_t>(T, 0x7FFFFF00ull);
+        return MK2_OK;
+    }
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
     const Plan p = make_plan(ctx, T, true, nchains);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
@@ -1407,7 +1420,8 @@ static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *
     // Everything on the device already: ONE kernel for the whole batch (mk2_fused.cuh) -- input words and state
     // never leave the SM.  It wants whole IV bytes, 10-byte IV records and 16-byte aligned arrays (what the
     // 128-bit record loads need); anything else takes the block pipeline below.
-    if (in_dev && out_dev && ctx->bulk_fused && ctx->row_staging != 1 && iv_bits % 8 == 0 &&
+    const bool small = ctx->small_batch && (N + 31) / 32 <= COOP_MAX_GROUPS;  // the warp-per-group kernels are quicker there
+    if (in_dev && out_dev && ctx->bulk_fused && !small && ctx->row_staging != 1 && iv_bits % 8 == 0 &&
         reinterpret_cast<uintptr_t>(keys) % 16 == 0 &&
         (iv_bits == 0 || (iv_stride == 10 && reinterpret_cast<uintptr_t>(ivs) % 16 == 0))) {
         const bool resume = N <= block_inst;  // as below: a single block leaves a state to resume from

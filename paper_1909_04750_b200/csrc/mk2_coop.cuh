@@ -191,5 +191,65 @@ gen_colmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict
     }
 }
 
+// 32 x 32 bit transpose across the warp: in: lane j holds word j; out: lane i holds column i (bit k = bit i of
+// word k).  Five butterfly stages (the log-step half-block swaps of bitslab.py:183-200 with the partner word in
+// another lane instead of another register).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane)
+{
+#pragma unroll
+    for (int st = 4; st >= 0; --st) {
+        const unsigned sh = 1u << st;
+        const uint32_t m = st == 4 ? 0xFFFF0000u : st == 3 ? 0xFF00FF00u : st == 2 ? 0xF0F0F0F0u : st == 1 ? 0xCCCCCCCCu : 0xAAAAAAAAu;
+        const uint32_t y = __shfl_xor_sync(FULL, x, sh);
+        x = (lane & sh) ? ((x & m) | ((y & m) >> sh)) : ((x & ~m) | ((y & ~m) << sh));
+    }
+    return x;
+}
+
+// Row-major keystream (kernels.py:604-621 layout; tmem::gen_rowmajor_kernel for small batches): every 32 clocks
+// the warp's 32 keystream words are bit-transposed across the lanes and lane i writes four bytes of instance
+// 32 g + i's row.  T is a multiple of 8.  LSB: first bit in the least significant position of a byte.
+template <bool LSB>
+__global__ void __launch_bounds__(32 * WARPS)
+gen_rowmajor_kernel(uint32_t *__restrict__ state, unsigned long long *__restrict__ acc, uint8_t *__restrict__ out, uint64_t pitch,
+                    uint64_t N, uint64_t G, uint64_t T)
+{
+    const unsigned lane = threadIdx.x & 31u;
+    const LaneTables t = make_tables(lane);
+    const bool word_stores = ((reinterpret_cast<uintptr_t>(out) | pitch) & 3u) == 0;
+    for (uint64_t g = (uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); g < G; g += (uint64_t)gridDim.x * WARPS) {
+        uint32_t r[PB], s[PB];
+        load_state(state, G, g, lane, r, s);
+        unsigned long long sum = 0;
+        const uint64_t row = 32 * g + lane;
+        uint8_t *dst = out + row * pitch;
+        for (uint64_t t0 = 0; t0 < T; t0 += 32) {
+            const int n = T - t0 < 32 ? (int)(T - t0) : 32;
+            uint32_t mine = 0;  // keystream word of clock t0 + lane
+#pragma unroll COOP_UNROLL
+            for (int j = 0; j < n; ++j) {
+                const uint32_t z = __shfl_sync(FULL, r[0] ^ s[0], 0);
+                if ((int)lane == j) mine = z;
+                clock<false, false>(r, s, 0u, t, lane);
+            }
+            sum += mine;
+            uint32_t w = warp_transpose32(mine, lane);  // bit k = z_{t0 + k} of instance 32 g + lane
+            if (!LSB) w = __byte_perm(__brev(w), 0u, 0x0123);  // MSB-first bytes in ascending address order (bitops.py:20-23)
+            if (row < N) {
+                uint8_t *p = dst + (t0 >> 3);
+                if (n == 32 && word_stores) {
+                    *reinterpret_cast<uint32_t *>(p) = w;
+                } else {
+                    for (int b = 0; b < (n >> 3); ++b) p[b] = (uint8_t)(w >> (8 * b));
+                }
+            }
+        }
+        store_state(state, G, g, lane, r, s);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) sum += __shfl_down_sync(FULL, sum, d);
+        if (lane == 0) acc[g] += sum;
+    }
+}
+
 }  // namespace coop
 }  // namespace mk2

@@ -9,6 +9,7 @@ only validates arguments, allocates buffers and passes pointers.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import numpy as np
@@ -41,6 +42,12 @@ def _ptr(buf) -> int:
     raise TypeError(f"unsupported buffer type {type(buf)!r}")
 
 
+# Contexts are created with the warp-per-group small-batch kernels enabled (csrc/mk2_coop.cuh).  MK2_SMALL_BATCH=0
+# in the environment, or this flag, makes new contexts use the thread-per-group throughput kernels at every size:
+# the GPU test suite runs itself both ways so that the edge cases of both kernel families stay covered.
+DEFAULT_SMALL_BATCH = os.environ.get("MK2_SMALL_BATCH", "1") != "0"
+
+
 class MickeyGenerator:
     """N independent MICKEY 2.0 instances on one B200 (32 per GPU thread)."""
 
@@ -51,6 +58,8 @@ class MickeyGenerator:
         self.device = int(device)
         self._knobs_touched = False   # hostmem's context pool only keeps contexts in their default configuration
         self._peak_groups = 0
+        if not DEFAULT_SMALL_BATCH:
+            self._ck(self._lib.mk2_set_small_batch(self._ctx, 0), "mk2_set_small_batch")
         if stream is not None:
             self.set_stream(stream)
 

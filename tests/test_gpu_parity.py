@@ -36,6 +36,20 @@ def torch_cuda():
     return torch
 
 
+@pytest.fixture(autouse=True, params=["small-batch-kernels", "throughput-kernels"])
+def kernel_family(request, monkeypatch):
+    """Every test of this file runs twice: with new contexts using the warp-per-group kernels for small batches
+    (the default, csrc/mk2_coop.cuh) and with the thread-per-group throughput kernels at every size -- most cases
+    here are small, and the tails, tile boundaries and staging modes of BOTH families must stay covered."""
+    from paper_1909_04750_b200 import generator, hostmem
+
+    monkeypatch.setattr(generator, "DEFAULT_SMALL_BATCH", request.param == "small-batch-kernels")
+    monkeypatch.setenv("MK2_SMALL_BATCH", "1" if request.param == "small-batch-kernels" else "0")   # child processes
+    hostmem.drop_idle_contexts()      # pooled contexts were created under the other setting
+    yield request.param
+    hostmem.drop_idle_contexts()
+
+
 def mats_of(pkg, recs):
     return [pkg.MickeyKeyIv(*golden_material(r)) for r in recs]
 
@@ -1066,6 +1080,7 @@ def test_small_batch_warp_per_group_kernels(pkg, oracle, N, T, iv_bits):
     ivs = rng.integers(0, 256, (N, 10), dtype=np.uint8)
     want = oracle.bulk_colmajor(keys, ivs, iv_bits, T + 40)
     with pkg.MickeyGenerator(0) as a, pkg.MickeyGenerator(0) as b:
+        a.set_small_batch(True)
         b.set_small_batch(False)
         wa = a.init_material(keys, ivs, iv_bits).generate_colmajor(T)
         wb = b.init_material(keys, ivs, iv_bits).generate_colmajor(T)
@@ -1076,10 +1091,22 @@ def test_small_batch_warp_per_group_kernels(pkg, oracle, N, T, iv_bits):
         b.set_small_batch(True)
         ma, mb = a.generate_colmajor(40), b.generate_colmajor(40)
         assert np.array_equal(ma, want[T:]) and np.array_equal(mb, want[T:]) and a.checksum() == b.checksum()
-        # row-major output of a state initialised by the small-batch init kernel
-        b.init_material(keys, ivs, iv_bits)
+        # row-major: the warp-per-group row kernel (32 x 32 bit transpose across the lanes), both byte orders, rows
+        # that are not 4-byte aligned, a resumed second piece; the throughput row kernel on the same state; and the
+        # one-shot bulk call, which takes the same small-batch route
         if T % 8 == 0:
-            assert np.array_equal(b.generate_rowmajor(T), oracle.bulk_rowmajor(keys, ivs, iv_bits, T))
+            rows = oracle.bulk_rowmajor(keys, ivs, iv_bits, T + 40)
+            assert np.array_equal(b.init_material(keys, ivs, iv_bits).generate_rowmajor(T), rows[:, : T // 8])
+            assert b.last_plan()[0] == 128
+            assert np.array_equal(b.generate_rowmajor(40), rows[:, T // 8:])
+            assert np.array_equal(a.init_material(keys, ivs, iv_bits).generate_rowmajor(T), rows[:, : T // 8])
+            odd = np.zeros((N, T // 8 + 3), np.uint8)
+            b.init_material(keys, ivs, iv_bits).generate_rowmajor(T, odd, pitch_bytes=odd.shape[1])
+            assert np.array_equal(odd[:, : T // 8], rows[:, : T // 8]) and not odd[:, T // 8:].any()
+            lsb = b.init_material(keys, ivs, iv_bits).generate_rowmajor(T, bit_order="lsb")
+            assert np.array_equal(lsb, np.packbits(np.unpackbits(rows[:, : T // 8], axis=1), axis=1, bitorder="little"))
+            got, csum = b.bulk_rowmajor(keys, ivs, iv_bits, T)
+            assert np.array_equal(got, rows[:, : T // 8]) and csum == oracle.checksum_material(keys, ivs, iv_bits, T)
 
 
 def test_c_abi_from_plain_c(c_abi_consumer):
@@ -1110,6 +1137,7 @@ def test_bulk_rowmajor_fused_kernel(pkg, oracle, N, T, iv_bits, pad, torch_cuda)
     want = oracle.bulk_rowmajor(keys[sample], ivs[sample], iv_bits, T)
     resumable = N <= 2 * 8 * torch.cuda.get_device_properties(0).multi_processor_count * 1024
     with pkg.MickeyGenerator(0) as gen:
+        gen.set_small_batch(False)                                 # batches of <= 2048 groups would take the warp-per-group kernels
         a = torch.zeros((N, T // 8 + pad), dtype=torch.uint8, device="cuda")
         _, ca = gen.bulk_rowmajor(dk, di, iv_bits, T, a)
         assert gen.last_kernel_launches == 1                       # the fused path ran
