@@ -125,3 +125,46 @@ def test_ragged_init_holds_late_lanes_with_five_extra_lop3_per_clock():
     counts = sorted(sum("LOP3" in t for _, t in body) for body in _innermost_clock_loops(ins, predicted - 2, predicted + 40))
     assert len(counts) >= 3, counts                      # pre-clock blocks, load blocks, masked load blocks
     assert predicted + 5 * K <= counts[-1] <= predicted + 5 * K + 14, (counts, predicted)
+
+
+def test_fused_one_shot_kernel_keeps_the_stand_alone_loops():
+    """fused::bulk_rowmajor_kernel (csrc/mk2_fused.cuh): its keystream loop is the tensor-memory row kernel's loop
+    (same LOP3 count, five tile stores per block, loop counters and tile address on the uniform datapath: at most one
+    R2UR, no spill -- what a branch that ptxas cannot prove warp-uniform around the loop would cost), and its load +
+    pre-clock phase is ONE loop of init blocks fed from tensor memory (LDTM), not two loops."""
+    lib = _native.lib()
+    k_row, row = lib.mk2_rblock(1), lib.mk2_lop3_per_block(1)
+    k_init, init = lib.mk2_rblock(2), lib.mk2_lop3_per_block(2)
+    kernels = _kernel_sass("fused20bulk_rowmajor_kernel")
+    assert len(kernels) == 2                                   # <ALIGNED16 = false / true>
+    for name, ins in kernels.items():
+        texts_all = [t for _, t in ins]
+        assert not [t for t in texts_all if re.search(r"\b(LDL|STL)\b", t)], name          # no spills anywhere
+        key = _innermost_clock_loops(ins, row - 2, row + 6)
+        assert len(key) == 1, (name, len(key))
+        texts = [t for _, t in key[0]]
+        assert sum(t.startswith("STTM") for t in texts) == k_row
+        assert sum(t.startswith("R2UR") for t in texts) <= 1 and not [t for t in texts if "WARPSYNC" in t]
+        assert sum(bool(re.match(r"(@!?U?P\d+\s+)?BRA", t)) for t in texts) == 1
+        load = _innermost_clock_loops(ins, init - 2, init + 12)
+        assert len(load) == 1, (name, len(load))               # load clocks and pre-clocks share one loop
+        texts = [t for _, t in load[0]]
+        assert sum(t.startswith("LDTM") for t in texts) == 1   # the next block's four input words
+        assert k_init == 4
+
+
+def test_small_batch_kernels_are_shuffle_and_lop3_only():
+    """coop::* (csrc/mk2_coop.cuh): a clock is LOP3s and warp shuffles -- no shared memory, no spills, and ~40 LOP3 +
+    11 SHFL per clock (eight clocks per loop iteration)."""
+    for part in ("coop19gen_colmajor_kernel", "coop19gen_rowmajor_kernel", "coop11init_kernel"):
+        kernels = _kernel_sass(part)
+        assert kernels, part
+        for name, ins in kernels.items():
+            texts = [t for _, t in ins]
+            assert not [t for t in texts if re.search(r"\b(LDL|STL|LDS|STS)\b", t)], name
+            loops = [b for b in _innermost_clock_loops(ins, 8 * 30, 8 * 60) if sum("SHFL" in t for _, t in b) >= 8 * 9]
+            assert loops, name
+            body = min(loops, key=len)
+            lop3 = sum("LOP3" in t for _, t in body)
+            shfl = sum("SHFL" in t for _, t in body)
+            assert 8 * 30 <= lop3 <= 8 * 52 and 8 * 9 <= shfl <= 8 * 13, (name, lop3, shfl)
