@@ -18,9 +18,19 @@ from paper_1909_04750_b200 import _native
 pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not available")
 
 
+_SASS = {}
+
+
+def _library_sass():
+    if "txt" not in _SASS:   # one disassembly of the library for the whole module
+        _native.lib()
+        _SASS["txt"] = subprocess.run(["cuobjdump", "-sass", str(_native.library_path())], stdout=subprocess.PIPE, text=True,
+                                      check=True).stdout
+    return _SASS["txt"]
+
+
 def _kernel_sass(name_part):
-    txt = subprocess.run(["cuobjdump", "-sass", str(_native.library_path())], stdout=subprocess.PIPE, text=True,
-                         check=True).stdout
+    txt = _library_sass()
     out = {}
     for chunk in re.split(r"\n\s*Function : ", txt)[1:]:
         name = chunk.split("\n", 1)[0].strip()
