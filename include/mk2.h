@@ -252,13 +252,16 @@ int mk2_host_free(void *p);
  * measured: it does not stay, 7.2 Tb/s against 10.4 -- kept as a documented
  * negative result).  Mode 3 on a MICKEY context behaves like 0. */
 int mk2_set_row_staging(mk2_ctx *ctx, int mode);
-/* Tuning knob: mk2_bulk_rowmajor with key/IV arrays AND output on the device runs
- * as one kernel (csrc/mk2_fused.cuh: records -> input words in tensor memory ->
+/* Tuning knob: mk2_bulk_rowmajor with key/IV arrays AND output on the device can
+ * run as one kernel (csrc/mk2_fused.cuh: records -> input words in tensor memory ->
  * load clocks -> pre-clocks -> keystream -> rows; neither the bitsliced material
  * nor the state passes through HBM) when the IV length is a whole number of bytes,
- * IV records are 10 bytes apart and both arrays are 16-byte aligned.  enable = 0
- * forces the pack / init / keystream kernels of the block pipeline (A/B, tests). */
-int mk2_set_bulk_fused(mk2_ctx *ctx, int enable);
+ * IV records are 10 bytes apart and both arrays are 16-byte aligned.
+ *   mode 1 (default): for init-dominated calls, T <= 1024 bits per instance
+ *          (BASELINE config 5); longer calls run pack + init + the persistent
+ *          keystream kernel over the whole batch, which is quicker there;
+ *   mode 2: whenever eligible;   mode 0: never (A/B, tests). */
+int mk2_set_bulk_fused(mk2_ctx *ctx, int mode);
 /* Tuning knob: small batches (up to 2048 groups = 65536 instances; the reference's
  * own calling unit is 64 lanes, kernels.py:189-200, cli.py:219-231) are initialised
  * and clocked column-major by warp-per-group kernels (csrc/mk2_coop.cuh: the 200

@@ -85,7 +85,8 @@ struct mk2_ctx {
     int row_staging = 0;                 // row-major staging tile: 0 = automatic, 1 = shared memory, 2 = tensor memory,
                                          // 3 = L2-resident scratch (Grain only)
     uint32_t *d_rowscratch = nullptr;    // staging mode 3: one 64 KiB tile per worker warp (lazy)
-    int bulk_fused = 1;                  // mk2_bulk_rowmajor with device buffers: 1 = the one-kernel path when eligible
+    int bulk_fused = 1;                  // mk2_bulk_rowmajor with device buffers, one-kernel path: 0 never, 1 automatic
+                                         // (init-dominated calls, T <= FUSED_MAX_CLOCKS), 2 whenever eligible
     int small_batch = 1;                 // 1 = warp-per-group kernels (mk2_coop.cuh) for G <= COOP_MAX_GROUPS
     int last_plan_block = 0;
     uint32_t last_plan_chunk = 0;
@@ -874,10 +875,11 @@ int mk2_set_small_batch(mk2_ctx *ctx, int enable)
     return MK2_OK;
 }
 
-int mk2_set_bulk_fused(mk2_ctx *ctx, int enable)
+int mk2_set_bulk_fused(mk2_ctx *ctx, int mode)
 {
     if (!ctx) return MK2_E_ARG;
-    ctx->bulk_fused = enable ? 1 : 0;
+    if (mode < 0 || mode > 2) return fail(ctx, MK2_E_ARG, "bulk fused mode must be 0 (never), 1 (automatic) or 2 (whenever eligible)");
+    ctx->bulk_fused = mode;
     return MK2_OK;
 }
 
@@ -1416,15 +1418,22 @@ static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *
     const Mem out_mem = classify(out);
     const bool in_dev = is_device_ptr(keys), out_dev = out_mem == Mem::Device;
     if (iv_bits && is_device_ptr(ivs) != in_dev) return fail(ctx, MK2_E_ARG, "keys and ivs must both be host or both be device pointers");
-    const uint64_t block_inst = 2ull * 8ull * (uint64_t)ctx->sm_count * 1024ull;  // two chains per worker warp
-    // Everything on the device already: ONE kernel for the whole batch (mk2_fused.cuh) -- input words and state
-    // never leave the SM.  It wants whole IV bytes, 10-byte IV records and 16-byte aligned arrays (what the
-    // 128-bit record loads need); anything else takes the block pipeline below.
+    uint64_t block_inst = 2ull * 8ull * (uint64_t)ctx->sm_count * 1024ull;  // two chains per worker warp
+    // Everything on the device already.  Init-dominated calls (T <= FUSED_MAX_CLOCKS; BASELINE config 5) run as ONE
+    // kernel for the whole batch (mk2_fused.cuh): input words and state never leave the SM.  It wants whole IV bytes,
+    // 10-byte IV records and 16-byte aligned arrays (what the 128-bit record loads need).  Keystream-dominated calls
+    // gain nothing from fusing the 260 init clocks and lose the chunk scheduler's short tail (measured, 2^24 x 65536:
+    // fused 590.7 ms, blocks 583.9, one block 579.6): they run as ONE block -- pack + init + persistent keystream
+    // kernel over all N, the state of all N on the device (48 B per instance with the packed input words) -- as long
+    // as that fits a modest budget; beyond it, and with host buffers, the block pipeline below.
+    constexpr uint64_t FUSED_MAX_CLOCKS = 1024, ONE_BLOCK_STATE_BUDGET = 16ull << 30;
     const bool small = ctx->small_batch && (N + 31) / 32 <= COOP_MAX_GROUPS;  // the warp-per-group kernels are quicker there
-    if (in_dev && out_dev && ctx->bulk_fused && !small && ctx->row_staging != 1 && iv_bits % 8 == 0 &&
+    if (in_dev && out_dev && N * 48 <= ONE_BLOCK_STATE_BUDGET) block_inst = std::max(block_inst, N);
+    if (in_dev && out_dev && (ctx->bulk_fused == 2 || (ctx->bulk_fused == 1 && T <= FUSED_MAX_CLOCKS)) && !small &&
+        ctx->row_staging != 1 && iv_bits % 8 == 0 &&
         reinterpret_cast<uintptr_t>(keys) % 16 == 0 &&
         (iv_bits == 0 || (iv_stride == 10 && reinterpret_cast<uintptr_t>(ivs) % 16 == 0))) {
-        const bool resume = N <= block_inst;  // as below: a single block leaves a state to resume from
+        const bool resume = N <= 2ull * 8ull * (uint64_t)ctx->sm_count * 1024ull;  // small enough to keep its state
         const uint64_t G = (N + 31) / 32;
         ctx->ready = false;
         if (resume) {

@@ -109,10 +109,11 @@ class MickeyGenerator:
         self._knobs_touched = True
         self._ck(self._lib.mk2_set_small_batch(self._ctx, int(bool(enable))), "mk2_set_small_batch")
 
-    def set_bulk_fused(self, enable: bool):
-        """Tuning knob: device-to-device bulk_rowmajor as one fused kernel (default) or as pack / init / keystream."""
+    def set_bulk_fused(self, mode):
+        """Tuning knob: device-to-device bulk_rowmajor as one fused kernel: 1 / True = automatic (init-dominated calls,
+        the default), 2 = whenever eligible, 0 / False = never (pack / init / keystream kernels)."""
         self._knobs_touched = True
-        self._ck(self._lib.mk2_set_bulk_fused(self._ctx, int(bool(enable))), "mk2_set_bulk_fused")
+        self._ck(self._lib.mk2_set_bulk_fused(self._ctx, int(mode)), "mk2_set_bulk_fused")
 
     def set_stage_bytes(self, nbytes: int):
         """Tuning knob: bytes per device staging tile when the output buffer is in host memory."""
