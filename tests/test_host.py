@@ -192,3 +192,23 @@ def test_grain_host_mirror(golden):
     src = (ROOT / "paper_1909_04750_b200" / "csrc" / "mk2_grain.cuh").read_text()
     for term in grain.NFSR_LINEAR_TAPS:
         assert f"b[C + {term}]" in src
+
+
+def test_bench_reference_arm_prints_one_json_line():
+    """bench.py --impl reference (the CPU arm the driver runs beside the GPU arm): stdout carries exactly one JSON
+    line with the contract's keys, whatever the libraries underneath print; `--cpu-kind port` = the oracle's C port
+    (the one place outside tests/ and smoke() that may execute oracle/), so it runs without the staged reference."""
+    import json
+    import subprocess
+    import sys
+
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--cpu-kind", "port", "--steps", "1",
+                          "--warmup", "0", "--cpu-seconds", "1"], capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "Tb/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "Tb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["metric"] == "keystream Tb/s, bitsliced MICKEY 2.0" and d["config"]["workload"].startswith("c2")
