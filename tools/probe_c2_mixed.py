@@ -17,7 +17,7 @@ lib = _native.lib()
 per_clock = lib.mk2_lop3_per_block(0) / lib.mk2_rblock(0)
 out = torch.empty((T, G), dtype=torch.int32, device="cuda")
 ideal = G * T * per_clock / peak * 1e3
-for block, chunk in ((0, 0), (224, 8192), (224, 4096), (224, 2048), (224, 1024), (256, 4096), (256, 2048), (192, 4096), (160, 4096), (0, 0)):
+for block, chunk in ((0, 0), (160, 4096), (160, 16384), (160, 32768), (192, 4096), (192, 8192), (192, 16384), (192, 32768), (224, 4096), (224, 16384), (0, 0)):
     gen.set_block_threads(block); gen.set_chunk_clocks(chunk)
     ms = []
     for _ in range(3):
