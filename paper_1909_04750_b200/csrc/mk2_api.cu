@@ -1282,14 +1282,18 @@ static int generate_colmajor_impl(mk2_ctx *ctx, uint64_t T, void *out, uint64_t 
         const size_t row_bytes = ctx->G * sizeof(uint32_t);
         HostTiles tiles(ctx, mem, T * row_bytes);
         // copy lanes work on 8 MiB sub-chunks: give them tiles of at least 128 MiB to spread over
-        const size_t target = tiles.pageable() && !ctx->stage_user ? std::max<size_t>(ctx->stage_target, size_t(128) << 20)
-                                                                    : ctx->stage_target;
+        // Pinned destinations: the D2H stream moves 128 MiB copies at 57.2 GB/s and 32 MiB ones at 56.85
+        // (profiles/r02b_probe_e2e_link.txt), but the link idles while the FIRST tile is generated -- so the tiles
+        // grow: 4 MiB, 8, ... up to 128 MiB (a 2 GiB call: 0.2 ms of fixed cost and 56.86 GB/s -> 0.07 ms and 57.1).
+        const bool ramp = !tiles.pageable() && !ctx->stage_user;
+        const size_t target = !ctx->stage_user ? std::max<size_t>(ctx->stage_target, size_t(128) << 20) : ctx->stage_target;
         const size_t want = std::max<size_t>(std::min<size_t>(target, T * row_bytes), row_bytes);
         if ((rc = ensure_stage(ctx, want))) return rc;
         if ((rc = tiles.prepare())) return rc;
-        const uint64_t chunk = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
-        for (uint64_t t0 = 0; t0 < T; t0 += chunk) {
-            const uint64_t tc = std::min(chunk, T - t0);
+        const uint64_t chunk_max = std::max<uint64_t>(1, ctx->stage_bytes / row_bytes);
+        uint64_t chunk = ramp ? std::min<uint64_t>(chunk_max, std::max<uint64_t>(1, (size_t(4) << 20) / row_bytes)) : chunk_max;
+        for (uint64_t t0 = 0, tc = 0; t0 < T; t0 += tc, chunk = std::min(chunk_max, 2 * chunk)) {
+            tc = std::min(chunk, T - t0);
             const int b = tiles.next();
             if ((rc = tiles.acquire(b))) return rc;
             if ((rc = launch_col(ctx, tc, static_cast<uint32_t *>(ctx->d_stage[b]), ctx->G))) return rc;
