@@ -1322,25 +1322,40 @@ static int rowmajor_to_host(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pit
     // move at two thirds of the rate of 1 KiB ones (profiles/r02_probe_host_buffers.txt), so rows are 1 KiB wide
     // and the chain block is halved instead (half the worker warps still generate at twice the link rate).
     const bool pageable = tiles.pageable();
-    const uint64_t tile_bytes = ROW_TILE_FACTOR * ctx->stage_target;
+    // Pinned destinations: a chain block of ONE chain per SM sub-partition and 256 MiB tiles.  A lone warp runs at
+    // twice the speed, so the call's first tile -- during which the link idles -- is ready in half the time, and half
+    // the worker warps still generate at several times the link rate.  Measured on one box, 2 GiB per call
+    // (tools/probe_e2e_row.py; before: two chains per sub-partition, 512 MiB tiles): 2^20 x 16384 bits 40.68 -> 39.61 ms,
+    // 2^24 x 1024 40.66 -> 40.14, 2^22 x 4096 41.66 -> 40.30.  Making the later tiles of a call wider (2-D copies of
+    // wider rows are more efficient in isolation) was measured too and loses 4-6% (MK2_ROW_WIDE = 2, 4, 8).
+    static const uint64_t env_factor = std::getenv("MK2_ROW_TILE_FACTOR") ? std::strtoull(std::getenv("MK2_ROW_TILE_FACTOR"), nullptr, 0) : 0;
+    static const uint64_t env_workers = std::getenv("MK2_ROW_WORKERS") ? std::strtoull(std::getenv("MK2_ROW_WORKERS"), nullptr, 0) : 0;
+    static const uint64_t env_wide = std::getenv("MK2_ROW_WIDE") ? std::strtoull(std::getenv("MK2_ROW_WIDE"), nullptr, 0) : 0;
+    const uint64_t tile_bytes = (env_factor ? env_factor : (pageable ? ROW_TILE_FACTOR : ROW_TILE_FACTOR / 2)) * ctx->stage_target;
     const uint64_t min_clocks = std::min<uint64_t>((T + 255) / 256 * 256, pageable ? 8192 : 4096);
-    const uint64_t workers = (pageable ? 4ull : 8ull) * (uint64_t)ctx->sm_count;
+    const uint64_t workers = (env_workers ? env_workers : 4ull) * (uint64_t)ctx->sm_count;
     const uint64_t want_chains = std::min<uint64_t>(2 * workers, std::max<uint64_t>(workers, tile_bytes / (min_clocks / 8) / 1024));
     const uint64_t block_chains = std::min<uint64_t>(chains, want_chains);
     const uint64_t block_rows = block_chains * 1024;
     uint64_t tc_max = std::max<uint64_t>(min_clocks, tile_bytes / block_rows / 32 * 256);
     tc_max = std::min<uint64_t>(tc_max, (T + 255) / 256 * 256);
+    // later tiles of a pinned call: up to `wide` x the first tile's width, within 1 GiB per staging buffer
+    const uint64_t wide = pageable || ctx->stage_user ? 1 : (env_wide ? env_wide : 1);
+    uint64_t tc_wide = std::min<uint64_t>(wide * tc_max, (T + 255) / 256 * 256);
+    while (tc_wide > tc_max && block_rows * (tc_wide / 8) > (size_t(1) << 30)) tc_wide -= 256;
     // a later block of a bulk call never needs larger staging buffers than the first one, but if it ever did the
     // copy lanes must be done with the old buffers before they are replaced (ensure_stage only knows the streams)
-    if (block_rows * (tc_max / 8) > ctx->stage_bytes && (rc = tiles.finish())) return rc;
-    if ((rc = ensure_stage(ctx, block_rows * (tc_max / 8)))) return rc;
+    if (block_rows * (tc_wide / 8) > ctx->stage_bytes && (rc = tiles.finish())) return rc;
+    if ((rc = ensure_stage(ctx, block_rows * (tc_wide / 8)))) return rc;
     if ((rc = tiles.prepare())) return rc;
+    bool first_tile = !ctx->copy_pending[0] && !ctx->copy_pending[1];  // nothing in flight: the link is idle
     for (uint64_t c0 = 0; c0 < chains; c0 += block_chains) {
         const uint64_t nch = std::min(block_chains, chains - c0);
         const uint64_t row0 = c0 * 1024;
         const uint64_t nrows = std::min<uint64_t>(nch * 1024, ctx->N - row0);
-        for (uint64_t t0 = 0; t0 < T; t0 += tc_max) {
-            const uint64_t tc = std::min(tc_max, T - t0);
+        for (uint64_t t0 = 0, tc = 0; t0 < T; t0 += tc) {
+            tc = std::min(first_tile ? tc_max : tc_wide, T - t0);
+            first_tile = false;
             const uint64_t sp = (tc / 8 + 15) / 16 * 16;  // staging pitch, 16-byte multiple
             const int b = tiles.next();
             if ((rc = tiles.acquire(b))) return rc;
