@@ -1527,8 +1527,17 @@ static int bulk_rowmajor_impl(mk2_ctx *ctx, const uint8_t *keys, const uint8_t *
     ctx->row_lsb = false;
     int launches = 0;
     uint64_t nblk = 0;
-    for (uint64_t row0 = 0; row0 < N; row0 += block_inst, ++nblk) {
-        const uint64_t n = std::min(block_inst, N - row0);
+    // Host buffers: the download cannot start before the first block's keys have been uploaded and its keystream
+    // generated, so for short keystreams the blocks GROW -- an eighth of the full size first, doubling (whole chains, so
+    // that block starts stay multiples of 64 instances): the link idles for 0.6 ms instead of 3 ms at the start of a
+    // call (2 GiB calls, tools/probe_e2e_row.py: 2^24 x 1024 bits 41.3 -> 40.4 ms, 2^22 x 4096 41.1 -> 40.4).  Long
+    // keystreams are the opposite case -- a small first block is a long serial job on a mostly idle GPU (2^20 x 16384:
+    // 39.9 -> 43.2 ms) -- and keep full blocks.
+    static const uint64_t env_ramp = std::getenv("MK2_BULK_RAMP") ? std::strtoull(std::getenv("MK2_BULK_RAMP"), nullptr, 0) : 0;
+    const uint64_t ramp = in_dev && out_dev ? 1 : (env_ramp ? env_ramp : (T <= 4096 ? 8 : 1));
+    uint64_t blk = std::max<uint64_t>(1024, block_inst / ramp / 1024 * 1024);
+    for (uint64_t row0 = 0, n = 0; row0 < N; row0 += n, ++nblk, blk = std::min(block_inst, 2 * blk)) {
+        n = std::min(blk, N - row0);
         ctx->last_launches = 0;
         const int i = (int)(nblk & 1);
         const uint8_t *dk, *di = nullptr;
