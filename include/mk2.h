@@ -250,7 +250,14 @@ int mk2_host_free(void *p);
  * (64 contiguous bytes per row and drain; slower overall);
  * 3 = the same 512-clock tiles in global scratch meant to stay in L2 (74 MB;
  * measured: it does not stay, 7.2 Tb/s against 10.4 -- kept as a documented
- * negative result).  Mode 3 on a MICKEY context behaves like 0. */
+ * negative result); 4 = the lone-warp experiments: row-major with four warps
+ * per SM, in-register bit transposes and the drain of a tile riding on the
+ * generation of the next one through a three-block ring (full 256-clock
+ * tiles, whole groups of 32 instances and 32-byte aligned rows only, other
+ * shapes fall back to 0; 10.5-10.6 Tb/s against 10.6-10.7), and column-major
+ * on an 80-word circular buffer with no realignment moves (T a multiple of
+ * 16; 12.3 Tb/s against 13.8: the 56 KB loop body is instruction-fetch
+ * bound).  Modes 3 and 4 on a MICKEY context behave like 0. */
 int mk2_set_row_staging(mk2_ctx *ctx, int mode);
 /* Tuning knob: mk2_bulk_rowmajor with key/IV arrays AND output on the device can
  * run as one kernel (csrc/mk2_fused.cuh: records -> input words in tensor memory ->

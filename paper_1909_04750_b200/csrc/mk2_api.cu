@@ -18,6 +18,7 @@
 #include "mk2_tmem.cuh"
 #include "mk2_grain.cuh"
 #include "mk2_grain_row64.cuh"
+#include "mk2_grain_ring.cuh"
 #include "mk2_fused.cuh"
 #include "mk2_coop.cuh"
 #include "mk2_seedgen.cuh"
@@ -310,9 +311,10 @@ struct Plan {
     bool tmem;        // row-major only: staging tile in tensor memory (mk2_tmem.cuh)
     bool row64;       // Grain row-major: 512-clock tiles, 64 bytes per row and drain (mk2_grain_row64.cuh)
     bool rowl2;       // ... with every warp's tile in L2-resident global scratch
+    bool ring;        // Grain row-major: four lone warps per SM, drains pipelined into the next tile (mk2_grain_ring.cuh)
 };
 
-Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
+Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains, bool ring_ok = false)
 {
     const uint64_t sms = (uint64_t)ctx->sm_count;
     Plan p{};
@@ -335,6 +337,11 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains)
     if (p.rowl2) {
         p.block = ctx->block_user ? ctx->block_user : BLOCK;
         p.tg = grain::row64::NGRP;
+    }
+    p.ring = ring_ok && rowmajor && ctx->cipher == 1 && ctx->row_staging == 4;
+    if (p.ring) {
+        p.block = grain::ring::THREADS;
+        p.tg = grain::ring::TILE_GROUPS;
     }
     const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::WIN : 1u);
     auto round_chunk = [&](uint64_t c) {
@@ -404,7 +411,11 @@ int launch_col(mk2_ctx *ctx, uint64_t T, uint32_t *out, uint64_t stride)
     const Plan p = make_plan(ctx, T, false, chains);
     int rc = launch_sched(ctx, p, chains);
     if (rc) return rc;
-    if (ctx->cipher == 1)
+    if (ctx->cipher == 1 && ctx->row_staging == 4 && T % grain::WIN == 0)
+        grain::gen_colmajor_circ_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc,
+                                                                             out, stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                                                                             ctx->d_slots, ctx->ring - 1, ctx->d_progress);
+    else if (ctx->cipher == 1)
         grain::gen_colmajor_kernel<<<p.grid, p.block, 0, ctx->stream>>>(ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc,
                                                                         out, stride, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
                                                                         ctx->d_slots, ctx->ring - 1, ctx->d_progress);
@@ -435,9 +446,24 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
         return MK2_OK;
     }
     const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (pitch % 16 == 0);
-    const Plan p = make_plan(ctx, T, true, nchains);  // chunks are whole staging tiles
+    // the lone-warp ring kernel takes only full tiles, whole groups and 32-byte aligned rows
+    const bool ring_ok = (reinterpret_cast<uintptr_t>(out) % 32 == 0) && (pitch % 32 == 0) && T % 256 == 0 && ctx->N % 32 == 0;
+    const Plan p = make_plan(ctx, T, true, nchains, ring_ok);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
+    if (p.ring) {
+        if (ctx->row_lsb)
+            grain::ring::gen_rowmajor_kernel<true><<<p.grid, p.block, grain::ring::SMEM_BYTES, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+        else
+            grain::ring::gen_rowmajor_kernel<false><<<p.grid, p.block, grain::ring::SMEM_BYTES, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+        CK(cudaGetLastError());
+        ctx->last_launches++;
+        return MK2_OK;
+    }
     if (p.rowl2) {
         if (!ctx->d_rowscratch)
             CK(cudaMalloc(&ctx->d_rowscratch, (size_t)ctx->sm_count * (BLOCK / 32) * grain::row64::L2TILE_BYTES_PER_WARP));
@@ -657,6 +683,12 @@ cudaError_t opt_in_row_kernels(int device)
     MK2_OPT_IN_GRAIN(16, 256);
 #undef MK2_OPT_IN_GRAIN
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grain::ring::gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 grain::ring::SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grain::ring::gen_rowmajor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 grain::ring::SMEM_BYTES);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(grain::row64::gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  grain::row64::SMEM_BYTES);
     if (e == cudaSuccess)
@@ -862,8 +894,9 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
 int mk2_set_row_staging(mk2_ctx *ctx, int mode)
 {
     if (!ctx) return MK2_E_ARG;
-    if (mode < 0 || mode > 3)
-        return fail(ctx, MK2_E_ARG, "row staging mode must be 0 (automatic), 1 (shared memory), 2 (tensor memory) or 3 (L2 scratch)");
+    if (mode < 0 || mode > 4)
+        return fail(ctx, MK2_E_ARG,
+                    "row staging mode must be 0 (automatic), 1 (shared memory), 2 (tensor memory), 3 (L2 scratch) or 4 (Grain ring)");
     ctx->row_staging = mode;
     return MK2_OK;
 }

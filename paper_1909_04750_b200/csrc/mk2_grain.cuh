@@ -41,42 +41,45 @@ constexpr unsigned L_AXORB_AND_C = 0x28; // (a ^ b) & c
 //   h = A ^ x2 D with A = x1 ^ x4 ^ t, t = x3 (x0 ^ x4), D = t ^ x3 ^ MAJ(x0, x1, x4)   (Shannon on x2)
 //   g = 12 linear taps ^ P1..P11 with the shared pairs b63b60, b37b33, b15b9, b52b45, b28b21; products
 //       of three or more taps are reduced to a pair and folded in as acc ^ (p & q).
-template <int C, bool INIT, int NW>
+template <int C, bool INIT, int NW, bool CIRC = false>
 __device__ __forceinline__ uint32_t step(uint32_t (&b)[NW], uint32_t (&s)[NW])
 {
-    static_assert(C + GB < NW, "window too short for this offset");
+    // CIRC: the registers are a circular buffer of GB words (bit i at clock t lives in word (t + i) mod GB, the
+    // feedback overwrites the word bit 0 leaves) instead of a sliding window: nothing ever has to be moved
+    static_assert(CIRC ? (NW == GB && C < GB) : (C + GB < NW), "window too short for this offset");
+    constexpr auto ix = [](int i) constexpr { return CIRC ? (C + i) % GB : C + i; };
     // ---- output z (grain.py:127-133)
-    const uint32_t x0 = s[C + 3], x1 = s[C + 25], x2 = s[C + 46], x3 = s[C + 64], x4 = b[C + 63];
+    const uint32_t x0 = s[ix(3)], x1 = s[ix(25)], x2 = s[ix(46)], x3 = s[ix(64)], x4 = b[ix(63)];
     const uint32_t t = lop3<L_AXORB_AND_C>(x0, x4, x3);
     const uint32_t m = lop3<L_MAJ>(x0, x1, x4);
     const uint32_t D = lop3<L_XOR3>(t, x3, m);
-    const uint32_t p1 = lop3<L_XOR3>(b[C + 1], b[C + 2], b[C + 4]);
-    const uint32_t p2 = lop3<L_XOR3>(b[C + 10], b[C + 31], b[C + 43]);
-    const uint32_t p3 = lop3<L_XOR3>(b[C + 56], t, x1);
+    const uint32_t p1 = lop3<L_XOR3>(b[ix(1)], b[ix(2)], b[ix(4)]);
+    const uint32_t p2 = lop3<L_XOR3>(b[ix(10)], b[ix(31)], b[ix(43)]);
+    const uint32_t p3 = lop3<L_XOR3>(b[ix(56)], t, x1);
     const uint32_t p4 = lop3<L_XOR3>(p1, p2, x4);
     const uint32_t p5 = lop3<L_A_XOR_BC>(p3, x2, D);
     const uint32_t z = p4 ^ p5;
     // ---- LFSR feedback f (grain.py:120-124)
-    const uint32_t f1 = lop3<L_XOR3>(s[C + 62], s[C + 51], s[C + 38]);
-    const uint32_t f2 = lop3<L_XOR3>(s[C + 23], s[C + 13], s[C + 0]);
+    const uint32_t f1 = lop3<L_XOR3>(s[ix(62)], s[ix(51)], s[ix(38)]);
+    const uint32_t f2 = lop3<L_XOR3>(s[ix(23)], s[ix(13)], s[ix(0)]);
     // ---- NFSR feedback g ^ s0 (grain.py:106-117)
-    const uint32_t P1 = b[C + 63] & b[C + 60], P2 = b[C + 37] & b[C + 33], P3 = b[C + 15] & b[C + 9];
-    const uint32_t pa = b[C + 52] & b[C + 45], pc = b[C + 28] & b[C + 21];
-    const uint32_t P5 = b[C + 33] & pc;
-    const uint32_t h6 = lop3<L_AND3>(b[C + 63], b[C + 45], b[C + 28]);
-    const uint32_t h7 = b[C + 60] & b[C + 52], h8 = b[C + 21] & b[C + 15], h9 = P1 & pa, h11 = pa & P2;
-    const uint32_t l1 = lop3<L_XOR3>(s[C + 0], b[C + 62], b[C + 60]);
-    const uint32_t l2 = lop3<L_XOR3>(b[C + 52], b[C + 45], b[C + 37]);
-    const uint32_t l3 = lop3<L_XOR3>(b[C + 33], b[C + 28], b[C + 21]);
-    const uint32_t l4 = lop3<L_XOR3>(b[C + 14], b[C + 9], b[C + 0]);
+    const uint32_t P1 = b[ix(63)] & b[ix(60)], P2 = b[ix(37)] & b[ix(33)], P3 = b[ix(15)] & b[ix(9)];
+    const uint32_t pa = b[ix(52)] & b[ix(45)], pc = b[ix(28)] & b[ix(21)];
+    const uint32_t P5 = b[ix(33)] & pc;
+    const uint32_t h6 = lop3<L_AND3>(b[ix(63)], b[ix(45)], b[ix(28)]);
+    const uint32_t h7 = b[ix(60)] & b[ix(52)], h8 = b[ix(21)] & b[ix(15)], h9 = P1 & pa, h11 = pa & P2;
+    const uint32_t l1 = lop3<L_XOR3>(s[ix(0)], b[ix(62)], b[ix(60)]);
+    const uint32_t l2 = lop3<L_XOR3>(b[ix(52)], b[ix(45)], b[ix(37)]);
+    const uint32_t l3 = lop3<L_XOR3>(b[ix(33)], b[ix(28)], b[ix(21)]);
+    const uint32_t l4 = lop3<L_XOR3>(b[ix(14)], b[ix(9)], b[ix(0)]);
     const uint32_t l5 = lop3<L_XOR3>(P1, P2, P3);
     uint32_t accA = lop3<L_XOR3>(l1, l2, l3);
     uint32_t accB = lop3<L_XOR3>(l4, l5, P5);
-    accA = lop3<L_A_XOR_BC>(accA, b[C + 60], pa);  // P4  = b60 b52 b45
-    accA = lop3<L_A_XOR_BC>(accA, h6, b[C + 9]);   // P6  = b63 b45 b28 b9
+    accA = lop3<L_A_XOR_BC>(accA, b[ix(60)], pa);  // P4  = b60 b52 b45
+    accA = lop3<L_A_XOR_BC>(accA, h6, b[ix(9)]);   // P6  = b63 b45 b28 b9
     accA = lop3<L_A_XOR_BC>(accA, h7, P2);         // P7  = b60 b52 b37 b33
     accA = lop3<L_A_XOR_BC>(accA, h8, P1);         // P8  = b63 b60 b21 b15
-    accB = lop3<L_A_XOR_BC>(accB, h9, b[C + 37]);  // P9  = b63 b60 b52 b45 b37
+    accB = lop3<L_A_XOR_BC>(accB, h9, b[ix(37)]);  // P9  = b63 b60 b52 b45 b37
     accB = lop3<L_A_XOR_BC>(accB, P5, P3);         // P10 = b33 b28 b21 b15 b9
     accB = lop3<L_A_XOR_BC>(accB, h11, pc);        // P11 = b52 b45 b37 b33 b28 b21
     uint32_t fl, fn;
@@ -87,8 +90,8 @@ __device__ __forceinline__ uint32_t step(uint32_t (&b)[NW], uint32_t (&s)[NW])
         fl = f1 ^ f2;
         fn = accA ^ accB;
     }
-    s[C + GB] = fl;
-    b[C + GB] = fn;
+    s[ix(GB)] = fl;
+    b[ix(GB)] = fn;
     return z;
 }
 
@@ -102,6 +105,59 @@ __device__ __forceinline__ void realign(uint32_t (&b)[NW], uint32_t (&s)[NW])
     }
 }
 
+// Realignment at the TOP of a window, through a copy ptxas cannot see through (an IMAD by a 1 read from constant
+// memory).  A plain b[i] = b[i + WIN] is copy-propagated into its readers and left without successors in the
+// loop body, so the list scheduler parks all ~160 moves behind the last LOP3 -- dead time for a warp that has its
+// sub-partition to itself.  As real producers of the window's first operands they are issued where they are
+// needed, between the LOP3s.  The state is then carried in words WIN .. WIN + 79 between windows.
+#ifndef MK2_GRAIN_TOP
+#define MK2_GRAIN_TOP 1
+#endif
+constexpr int OFF = MK2_GRAIN_TOP ? WIN : 0;  // where the state sits between two windows
+__constant__ uint32_t opaque_one = 1u;
+__device__ __forceinline__ uint32_t opaque_copy(uint32_t x)
+{
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(d) : "r"(x), "r"(opaque_one));
+    return d;
+}
+template <int NW>
+__device__ __forceinline__ void realign_top(uint32_t (&b)[NW], uint32_t (&s)[NW])
+{
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        b[i] = opaque_copy(b[i + WIN]);
+        s[i] = opaque_copy(s[i + WIN]);
+    }
+}
+// window prologue / epilogue of the keystream loops, and the switch between the two conventions around a tail
+template <int NW>
+__device__ __forceinline__ void window_begin(uint32_t (&b)[NW], uint32_t (&s)[NW])
+{
+    if constexpr (MK2_GRAIN_TOP) realign_top(b, s);
+}
+template <int NW>
+__device__ __forceinline__ void window_end(uint32_t (&b)[NW], uint32_t (&s)[NW])
+{
+    if constexpr (!MK2_GRAIN_TOP) realign<WIN>(b, s);
+}
+template <int NW>
+__device__ __forceinline__ void tail_begin(uint32_t (&b)[NW], uint32_t (&s)[NW])  // state to words 0 .. 79
+{
+    if constexpr (MK2_GRAIN_TOP) realign<WIN>(b, s);
+}
+template <int NW>
+__device__ __forceinline__ void tail_end(uint32_t (&b)[NW], uint32_t (&s)[NW])  // and back to OFF .. OFF + 79
+{
+    if constexpr (MK2_GRAIN_TOP) {
+#pragma unroll
+        for (int i = GB - 1; i >= 0; --i) {
+            b[i + WIN] = b[i];
+            s[i + WIN] = s[i];
+        }
+    }
+}
+
 template <int Lo, int Hi, class F>
 __device__ __forceinline__ void static_for_up(F &&f)
 {
@@ -112,36 +168,38 @@ __device__ __forceinline__ void static_for_up(F &&f)
 }
 
 // state[160][G]: words 0..79 = NFSR, 80..159 = LFSR (same coalesced layout as MICKEY's)
-template <int NW>
+template <int O = 0, int NW>
 __device__ __forceinline__ void load_state(const uint32_t *state, const unsigned long long *acc, uint64_t G, uint64_t g,
                                            uint32_t (&b)[NW], uint32_t (&s)[NW], unsigned long long &a)
 {
     const uint32_t *p = state + g;
+    constexpr int o = O;  // first state word: OFF in the sliding-window kernels of this file
 #pragma unroll
     for (int i = 0; i < GB; ++i) {
-        b[i] = __ldcg(p);
+        b[o + i] = __ldcg(p);
         bump(p, G);
     }
 #pragma unroll
     for (int i = 0; i < GB; ++i) {
-        s[i] = __ldcg(p);
+        s[o + i] = __ldcg(p);
         bump(p, G);
     }
     a = __ldcg(acc + g);
 }
-template <int NW>
+template <int O = 0, int NW>
 __device__ __forceinline__ void store_state(uint32_t *state, unsigned long long *acc, uint64_t G, uint64_t g,
                                             const uint32_t (&b)[NW], const uint32_t (&s)[NW], unsigned long long a)
 {
     const uint32_t *p = state + g;
+    constexpr int o = O;  // first state word: OFF in the sliding-window kernels of this file
 #pragma unroll
     for (int i = 0; i < GB; ++i) {
-        __stcg(const_cast<uint32_t *>(p), b[i]);
+        __stcg(const_cast<uint32_t *>(p), b[o + i]);
         bump(p, G);
     }
 #pragma unroll
     for (int i = 0; i < GB; ++i) {
-        __stcg(const_cast<uint32_t *>(p), s[i]);
+        __stcg(const_cast<uint32_t *>(p), s[o + i]);
         bump(p, G);
     }
     st_release_u64(acc + g, a);
@@ -222,7 +280,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
         if (g < G) {
             uint32_t b[GW], s[GW];
             unsigned long long a;
-            load_state(state, acc, G, g, b, s, a);
+            load_state<OFF>(state, acc, G, g, b, s, a);
 #ifndef MK2_GRAIN_COL_FMA
 #define MK2_GRAIN_COL_FMA 1
 #endif
@@ -243,21 +301,26 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 HalfSums hs;
 #pragma unroll 1
                 for (; u + WIN <= nseg; u += WIN) {
+                    window_begin(b, s);
                     static_for_up<0, WIN>([&](auto ic) {
                         const uint32_t z = step<decltype(ic)::value, false>(b, s);
                         base[idx] = z;
                         idx += stride32;
                         hs.add(z);
                     });
-                    realign<WIN>(b, s);
+                    window_end(b, s);
                 }
+                if (u < nseg) {
+                    tail_begin(b, s);
 #pragma unroll 1
-                for (; u < nseg; ++u) {
-                    const uint32_t z = step<0, false>(b, s);
-                    base[idx] = z;
-                    idx += stride32;
-                    hs.add(z);
-                    realign<1>(b, s);
+                    for (; u < nseg; ++u) {
+                        const uint32_t z = step<0, false>(b, s);
+                        base[idx] = z;
+                        idx += stride32;
+                        hs.add(z);
+                        realign<1>(b, s);
+                    }
+                    tail_end(b, s);
                 }
                 hs.fold(a);
                 base += (uint64_t)nseg * stride;
@@ -268,24 +331,124 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             uint64_t t = 0;
 #pragma unroll 1
             for (; t + WIN <= tc; t += WIN) {
+                window_begin(b, s);
                 static_for_up<0, WIN>([&](auto ic) {
                     const uint32_t z = step<decltype(ic)::value, false>(b, s);
                     *p = z;
                     p += stride;
                     acc_add(a, z);
                 });
-                realign<WIN>(b, s);
+                window_end(b, s);
             }
+            if (t < tc) {
+                tail_begin(b, s);
 #pragma unroll 1
-            for (; t < tc; ++t) {
-                const uint32_t z = step<0, false>(b, s);
-                *p = z;
-                p += stride;
-                acc_add(a, z);
-                realign<1>(b, s);
+                for (; t < tc; ++t) {
+                    const uint32_t z = step<0, false>(b, s);
+                    *p = z;
+                    p += stride;
+                    acc_add(a, z);
+                    realign<1>(b, s);
+                }
+                tail_end(b, s);
             }
 #endif
-            store_state(state_out, acc_out, G, g, b, s, a);
+            store_state<OFF>(state_out, acc_out, G, g, b, s, a);
+        }
+        sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Circular-buffer clocking: 80 words per register and NO realignment.  Clock t at compile-time phase
+// P = t mod 80 reads word (P + tap) mod 80 and overwrites word P, so the loop body is five 16-clock segments
+// (phases 0, 16, .. 64) dispatched by a slot counter; a chunk may stop after any segment and the state is
+// parked from the rotation it is left in.  What it buys: the 164 register moves per 16 clocks of the sliding
+// window are gone (a lone warp per sub-partition cannot overlap them with its LOP3s) and 32 registers are
+// free.  What it costs: a 5 x longer body (instruction cache).
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ void store_state_rot(uint32_t *state, unsigned long long *acc, uint64_t G, uint64_t g,
+                                                const uint32_t (&b)[GB], const uint32_t (&s)[GB], unsigned long long a)
+{
+    const uint32_t *p = state + g;
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        __stcg(const_cast<uint32_t *>(p), b[(R + i) % GB]);
+        bump(p, G);
+    }
+#pragma unroll
+    for (int i = 0; i < GB; ++i) {
+        __stcg(const_cast<uint32_t *>(p), s[(R + i) % GB]);
+        bump(p, G);
+    }
+    st_release_u64(acc + g, a);
+}
+__device__ __forceinline__ void store_state_slot(uint32_t slot, uint32_t *state, unsigned long long *acc, uint64_t G, uint64_t g,
+                                                 const uint32_t (&b)[GB], const uint32_t (&s)[GB], unsigned long long a)
+{
+    switch (slot) {
+    case 0: store_state_rot<0>(state, acc, G, g, b, s, a); break;
+    case 1: store_state_rot<16>(state, acc, G, g, b, s, a); break;
+    case 2: store_state_rot<32>(state, acc, G, g, b, s, a); break;
+    case 3: store_state_rot<48>(state, acc, G, g, b, s, a); break;
+    default: store_state_rot<64>(state, acc, G, g, b, s, a); break;
+    }
+}
+
+// Column-major keystream on the circular buffer (T a multiple of 16 clocks).
+__global__ void __launch_bounds__(BLOCK, 1)
+gen_colmajor_circ_kernel(const uint32_t *state, const unsigned long long *acc, uint32_t *state_out,
+                         unsigned long long *acc_out, uint32_t *__restrict__ out, uint64_t stride, uint64_t G, uint64_t T,
+                         uint32_t chunk, uint32_t chunks_per_chain, SchedQueue *q, unsigned long long *slots, uint32_t mask,
+                         uint32_t *progress)
+{
+    uint32_t chain;
+    while (sched_pop(q, slots, mask, chain)) {
+        const uint32_t k = __ldcg(progress + chain);
+        const uint64_t g = (uint64_t)chain * 32 + (threadIdx.x & 31u);
+        const uint64_t t0 = (uint64_t)k * chunk;
+        const uint64_t tc = T - t0 < chunk ? T - t0 : chunk;
+        if (g < G) {
+            uint32_t b[GB], s[GB];
+            unsigned long long a;
+            load_state(state, acc, G, g, b, s, a);
+            uint32_t *base = out + t0 * stride + g;
+            const uint32_t stride32 = (uint32_t)stride;  // host side guarantees stride < 2^30
+            uint32_t seg_max = 0xFFFFFFFFu / stride32;
+            if (seg_max > HALFSUM_MAX_WORDS) seg_max = HALFSUM_MAX_WORDS;
+            seg_max -= seg_max % WIN;
+            uint32_t slot = 0;
+            uint64_t t = 0;
+#pragma unroll 1
+            while (t < tc) {
+                const uint32_t nseg = tc - t < seg_max ? (uint32_t)(tc - t) : seg_max;
+                uint32_t idx = 0;
+                HalfSums hs;
+                auto seg = [&](auto pc) {
+                    static_for_up<0, WIN>([&](auto ic) {
+                        const uint32_t z = step<decltype(pc)::value + decltype(ic)::value, false, GB, true>(b, s);
+                        base[idx] = z;
+                        idx += stride32;
+                        hs.add(z);
+                    });
+                };
+#pragma unroll 1
+                for (uint32_t left = nseg / WIN; left; --left) {
+                    switch (slot) {
+                    case 0: seg(std::integral_constant<int, 0>{}); break;
+                    case 1: seg(std::integral_constant<int, 16>{}); break;
+                    case 2: seg(std::integral_constant<int, 32>{}); break;
+                    case 3: seg(std::integral_constant<int, 48>{}); break;
+                    default: seg(std::integral_constant<int, 64>{}); break;
+                    }
+                    slot = slot == 4 ? 0 : slot + 1;
+                }
+                hs.fold(a);
+                base += (uint64_t)nseg * stride;
+                t += nseg;
+            }
+            store_state_slot(slot, state_out, acc_out, G, g, b, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }
@@ -310,7 +473,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
         if (g < G) {
             uint32_t b[GW], s[GW];
             unsigned long long a;
-            load_state(state, acc, G, g, b, s, a);
+            load_state<OFF>(state, acc, G, g, b, s, a);
             uint8_t *rows = out + 32 * (g - (uint64_t)chain_base * 32) * pitch + (c0 >> 3);
             const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;
 #pragma unroll 1
@@ -321,6 +484,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 HalfSums hs;  // checksum on the FMA pipe; a tile is at most 256 words
 #pragma unroll 1
                 for (; t + WIN <= nclk; t += WIN) {
+                    window_begin(b, s);
                     static_for_up<0, WIN>([&](auto ic) {
                         constexpr int c = decltype(ic)::value;
                         const uint32_t z = step<c, false>(b, s);
@@ -328,20 +492,24 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                         hs.add(z);
                     });
                     zp += WIN * ts;
-                    realign<WIN>(b, s);
+                    window_end(b, s);
                 }
+                if (t < nclk) {
+                    tail_begin(b, s);
 #pragma unroll 1
-                for (; t < nclk; ++t) {
-                    const uint32_t z = step<0, false>(b, s);
-                    *zp = z;
-                    zp += ts;
-                    hs.add(z);
-                    realign<1>(b, s);
+                    for (; t < nclk; ++t) {
+                        const uint32_t z = step<0, false>(b, s);
+                        *zp = z;
+                        zp += ts;
+                        hs.add(z);
+                        realign<1>(b, s);
+                    }
+                    tail_end(b, s);
                 }
                 hs.fold(a);
                 row_drain<ALIGNED16, TG, TS, LSB, GRAIN_STORE_POLICY>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
             }
-            store_state(state_out, acc_out, G, g, b, s, a);
+            store_state<OFF>(state_out, acc_out, G, g, b, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }

@@ -191,7 +191,7 @@ def test_grain_host_mirror(golden):
         grain.pack_materials([m] * 33, 32)
     src = (ROOT / "paper_1909_04750_b200" / "csrc" / "mk2_grain.cuh").read_text()
     for term in grain.NFSR_LINEAR_TAPS:
-        assert f"b[C + {term}]" in src
+        assert f"b[ix({term})]" in src   # ix(i) = window offset (or circular index) of bit i
 
 
 def test_bench_reference_arm_prints_one_json_line():
