@@ -23,9 +23,13 @@ namespace grain {
 
 constexpr int GB = 80;           // bits per register (grain.py:29)
 #ifndef MK2_GRAIN_STORE_POLICY
-#define MK2_GRAIN_STORE_POLICY 2
+#define MK2_GRAIN_STORE_POLICY 3
 #endif
-constexpr int GRAIN_STORE_POLICY = MK2_GRAIN_STORE_POLICY;  // row stores: 1 = 2 x 16 B, 2 = 1 x 32 B, both L2 evict_last
+constexpr int GRAIN_STORE_POLICY = MK2_GRAIN_STORE_POLICY;  // row stores: 1 = 2 x 16 B, 2 = 1 x 32 B, both L2 evict_last;
+                                                            // 3 = 1 x 32 B, evict_last except for the sector that completes a 128-byte line
+#ifndef MK2_GRAIN_ROW_FUSED_T
+#define MK2_GRAIN_ROW_FUSED_T 1
+#endif
 constexpr int WIN = 16;          // clocks per window realignment
 constexpr int GW = GB + WIN;     // window length
 constexpr int INIT_CLOCKS = 160; // grain.py:30
@@ -482,6 +486,36 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 uint32_t *zp = col;
                 int t = 0;
                 HalfSums hs;  // checksum on the FMA pipe; a tile is at most 256 words
+#if MK2_GRAIN_ROW_FUSED_T
+                if (nclk == 8 * TG) {
+                    // full tile: the 8 x 32 bit transposes run in registers on each 8-clock group as it is
+                    // produced, so the drain has no load / transpose / store pass over the tile
+#pragma unroll 1
+                    for (; t < nclk; t += WIN) {
+                        window_begin(b, s);
+                        uint32_t zz[WIN];
+                        static_for_up<0, WIN>([&](auto ic) {
+                            constexpr int c = decltype(ic)::value;
+                            zz[c] = step<c, false>(b, s);
+                            hs.add(zz[c]);
+                        });
+#pragma unroll
+                        for (int h = 0; h < WIN / 8; ++h) {
+                            uint32_t z[8];
+#pragma unroll
+                            for (int m = 0; m < 8; ++m) z[LSB ? m : 7 - m] = zz[8 * h + m];
+                            transpose8x32(z);
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk) zp[(8 * h + kk) * ts] = z[kk];
+                        }
+                        zp += WIN * ts;
+                        window_end(b, s);
+                    }
+                    hs.fold(a);
+                    row_drain<ALIGNED16, TG, TS, LSB, GRAIN_STORE_POLICY, true>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
+                    continue;
+                }
+#endif
 #pragma unroll 1
                 for (; t + WIN <= nclk; t += WIN) {
                     window_begin(b, s);

@@ -814,18 +814,32 @@ __device__ __forceinline__ void store32_keep(uint8_t *p, const uint32_t (&v)[8])
                  : "memory");
 }
 
+// The same store, but the sector that COMPLETES a 128-byte line (address bits 6:5 = 3) is written evict_first:
+// a complete line has nothing left to wait for in L2 and should make room for the open ones.
+__device__ __forceinline__ void store32_line(uint8_t *p, const uint32_t (&v)[8])
+{
+    unsigned long long keep, go;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(go));
+    const unsigned long long pol = (reinterpret_cast<uintptr_t>(p) & 96) == 96 ? go : keep;
+    asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(pol)
+                 : "memory");
+}
+
 // Drain of one staging tile (ngrp 8-clock groups of keystream words in the thread's smem
 // column `col`, stride TS) into the instance rows at `dst`.  Shared by every cipher's
 // row-major kernel.  LSB selects the byte packing: first bit in the MSB (library default,
 // bitops.py:20-23) or in the LSB (Grain's published convention, grain.py:13-16).
-template <bool ALIGNED16, int TG, int TS, bool LSB, int STORE_POLICY = 0>
+template <bool ALIGNED16, int TG, int TS, bool LSB, int STORE_POLICY = 0, bool PRE_TRANSPOSED = false>
 __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t pitch, int ngrp, uint64_t nrows)
 {
     constexpr uint32_t ts = TS;
     // ---- pass 1: bit transposes, in place in the smem column; the next group's 8 words
     // are fetched while the current group is transposed (a lone warp has nobody else to
-    // hide the LDS latency behind)
-    {
+    // hide the LDS latency behind).  PRE_TRANSPOSED: the producer already stored the
+    // transposed words of every group (Grain's full tiles).
+    if constexpr (!PRE_TRANSPOSED) {
         uint32_t nx[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) nx[m] = col[m * ts];
@@ -846,7 +860,7 @@ __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t 
     }
     // ---- pass 2: TG bytes (or the tail) per instance row, 16 bytes per store; the two
     // halves of a 32-byte sector are stored back to back so they merge in L2
-    if (STORE_POLICY == 2 && TG == 32 && ALIGNED16 && ngrp == TG && nrows == 32 &&
+    if (STORE_POLICY >= 2 && TG == 32 && ALIGNED16 && ngrp == TG && nrows == 32 &&
         ((reinterpret_cast<uintptr_t>(dst) | pitch) & 31) == 0) {
         // whole 32-byte sectors in one store each
 #pragma unroll 1
@@ -862,7 +876,8 @@ __device__ __forceinline__ void row_drain(uint32_t *col, uint8_t *dst, uint64_t 
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 const uint32_t v[8] = {y[0][qq], y[1][qq], y[2][qq], y[3][qq], y[4][qq], y[5][qq], y[6][qq], y[7][qq]};
-                store32_keep(dst + (uint64_t)(8 * qq + kk) * pitch, v);
+                if constexpr (STORE_POLICY == 3) store32_line(dst + (uint64_t)(8 * qq + kk) * pitch, v);
+                else store32_keep(dst + (uint64_t)(8 * qq + kk) * pitch, v);
             }
         }
     } else if (ALIGNED16 && ngrp == TG && nrows == 32) {

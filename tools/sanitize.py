@@ -66,4 +66,16 @@ with grain.GrainGenerator(0) as gg:
     gg.set_row_staging(2)
     grow = gg.init_material(gk, gi).generate_rowmajor(1024 + 136)
 assert np.array_equal(grow, orc.grain_bulk_rowmajor(gk, gi, 1024 + 136))
+# Grain: default kernels (top-of-window realignment) in both layouts with a tail, and the mode-4 kernels (lone-warp
+# ring kernel with three tiles per chunk + a one-tile chunk; circular-buffer column-major kernel)
+with grain.GrainGenerator(0) as gg:
+    gcol = gg.init_material(gk, gi).generate_colmajor(200)
+    grow2 = gg.init_material(gk, gi).generate_rowmajor(392)
+    gg.set_row_staging(4)
+    gg.set_chunk_clocks(768)
+    ring = gg.init_material(gk[:1280], gi[:1280]).generate_rowmajor(1024)
+    circ = gg.init_material(gk, gi).generate_colmajor(208)
+assert np.array_equal(gcol, orc.grain_bulk_colmajor(gk, gi, 200)) and np.array_equal(grow2, orc.grain_bulk_rowmajor(gk, gi, 392))
+assert np.array_equal(ring, orc.grain_bulk_rowmajor(gk[:1280], gi[:1280], 1024))
+assert np.array_equal(circ, orc.grain_bulk_colmajor(gk, gi, 208))
 print("sanitize run ok")
