@@ -749,6 +749,15 @@ int mk2_create(int device, mk2_ctx **out)
     if (!c) return fail(nullptr, MK2_E_NOMEM, "out of host memory");
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    // experiment knob (tools/probe_grain_l2_persist.sh): L2 set-aside for persisting (evict_last) lines, in MiB
+    if (const char *v = std::getenv("MK2_L2_PERSIST_MB")) {
+        const size_t want = std::min<size_t>((size_t)std::strtoull(v, nullptr, 0) << 20, (size_t)prop.persistingL2CacheMaxSize);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        size_t got = 0;
+        cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+        std::fprintf(stderr, "mk2: persisting L2 set-aside %zu MiB (max %d MiB, L2 %d MiB)\n", got >> 20,
+                     prop.persistingL2CacheMaxSize >> 20, prop.l2CacheSize >> 20);
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
