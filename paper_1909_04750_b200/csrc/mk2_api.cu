@@ -343,7 +343,7 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains, b
         p.block = grain::ring::THREADS;
         p.tg = grain::ring::TILE_GROUPS;
     }
-    const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::WIN : 1u);
+    const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::CWIN : 1u);
     auto round_chunk = [&](uint64_t c) {
         c = std::max<uint64_t>(c, granule);
         c = (c + granule - 1) / granule * granule;

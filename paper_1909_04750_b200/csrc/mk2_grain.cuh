@@ -118,6 +118,13 @@ __device__ __forceinline__ void realign(uint32_t (&b)[NW], uint32_t (&s)[NW])
 #define MK2_GRAIN_TOP 1
 #endif
 constexpr int OFF = MK2_GRAIN_TOP ? WIN : 0;  // where the state sits between two windows
+// the column-major loop may use a longer window (it has registers to spare): half the copies per clock
+#ifndef MK2_GRAIN_COL_WIN
+#define MK2_GRAIN_COL_WIN 32
+#endif
+constexpr int CWIN = MK2_GRAIN_COL_WIN;
+constexpr int CGW = GB + CWIN;
+constexpr int COFF = MK2_GRAIN_TOP ? CWIN : 0;
 __constant__ uint32_t opaque_one = 1u;
 __device__ __forceinline__ uint32_t opaque_copy(uint32_t x)
 {
@@ -125,39 +132,39 @@ __device__ __forceinline__ uint32_t opaque_copy(uint32_t x)
     asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(d) : "r"(x), "r"(opaque_one));
     return d;
 }
-template <int NW>
+template <int W = WIN, int NW>
 __device__ __forceinline__ void realign_top(uint32_t (&b)[NW], uint32_t (&s)[NW])
 {
 #pragma unroll
     for (int i = 0; i < GB; ++i) {
-        b[i] = opaque_copy(b[i + WIN]);
-        s[i] = opaque_copy(s[i + WIN]);
+        b[i] = opaque_copy(b[i + W]);
+        s[i] = opaque_copy(s[i + W]);
     }
 }
 // window prologue / epilogue of the keystream loops, and the switch between the two conventions around a tail
-template <int NW>
+template <int W = WIN, int NW>
 __device__ __forceinline__ void window_begin(uint32_t (&b)[NW], uint32_t (&s)[NW])
 {
-    if constexpr (MK2_GRAIN_TOP) realign_top(b, s);
+    if constexpr (MK2_GRAIN_TOP) realign_top<W>(b, s);
 }
-template <int NW>
+template <int W = WIN, int NW>
 __device__ __forceinline__ void window_end(uint32_t (&b)[NW], uint32_t (&s)[NW])
 {
-    if constexpr (!MK2_GRAIN_TOP) realign<WIN>(b, s);
+    if constexpr (!MK2_GRAIN_TOP) realign<W>(b, s);
 }
-template <int NW>
+template <int W = WIN, int NW>
 __device__ __forceinline__ void tail_begin(uint32_t (&b)[NW], uint32_t (&s)[NW])  // state to words 0 .. 79
 {
-    if constexpr (MK2_GRAIN_TOP) realign<WIN>(b, s);
+    if constexpr (MK2_GRAIN_TOP) realign<W>(b, s);
 }
-template <int NW>
-__device__ __forceinline__ void tail_end(uint32_t (&b)[NW], uint32_t (&s)[NW])  // and back to OFF .. OFF + 79
+template <int W = WIN, int NW>
+__device__ __forceinline__ void tail_end(uint32_t (&b)[NW], uint32_t (&s)[NW])  // and back to W .. W + 79
 {
     if constexpr (MK2_GRAIN_TOP) {
 #pragma unroll
         for (int i = GB - 1; i >= 0; --i) {
-            b[i + WIN] = b[i];
-            s[i + WIN] = s[i];
+            b[i + W] = b[i];
+            s[i + W] = s[i];
         }
     }
 }
@@ -282,9 +289,9 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
         const uint64_t t0 = (uint64_t)k * chunk;
         const uint64_t tc = T - t0 < chunk ? T - t0 : chunk;
         if (g < G) {
-            uint32_t b[GW], s[GW];
+            uint32_t b[CGW], s[CGW];
             unsigned long long a;
-            load_state<OFF>(state, acc, G, g, b, s, a);
+            load_state<COFF>(state, acc, G, g, b, s, a);
 #ifndef MK2_GRAIN_COL_FMA
 #define MK2_GRAIN_COL_FMA 1
 #endif
@@ -296,7 +303,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             const uint32_t stride32 = (uint32_t)stride;  // host side guarantees stride < 2^30
             uint32_t seg_max = 0xFFFFFFFFu / stride32;
             if (seg_max > HALFSUM_MAX_WORDS) seg_max = HALFSUM_MAX_WORDS;
-            if (seg_max > WIN) seg_max -= seg_max % WIN;
+            if (seg_max > CWIN) seg_max -= seg_max % CWIN;
             uint64_t t = 0;
 #pragma unroll 1
             while (t < tc) {
@@ -304,18 +311,18 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 uint32_t idx = 0, u = 0;
                 HalfSums hs;
 #pragma unroll 1
-                for (; u + WIN <= nseg; u += WIN) {
-                    window_begin(b, s);
-                    static_for_up<0, WIN>([&](auto ic) {
+                for (; u + CWIN <= nseg; u += CWIN) {
+                    window_begin<CWIN>(b, s);
+                    static_for_up<0, CWIN>([&](auto ic) {
                         const uint32_t z = step<decltype(ic)::value, false>(b, s);
                         base[idx] = z;
                         idx += stride32;
                         hs.add(z);
                     });
-                    window_end(b, s);
+                    window_end<CWIN>(b, s);
                 }
                 if (u < nseg) {
-                    tail_begin(b, s);
+                    tail_begin<CWIN>(b, s);
 #pragma unroll 1
                     for (; u < nseg; ++u) {
                         const uint32_t z = step<0, false>(b, s);
@@ -324,7 +331,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                         hs.add(z);
                         realign<1>(b, s);
                     }
-                    tail_end(b, s);
+                    tail_end<CWIN>(b, s);
                 }
                 hs.fold(a);
                 base += (uint64_t)nseg * stride;
@@ -334,18 +341,18 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             uint32_t *p = out + t0 * stride + g;
             uint64_t t = 0;
 #pragma unroll 1
-            for (; t + WIN <= tc; t += WIN) {
-                window_begin(b, s);
-                static_for_up<0, WIN>([&](auto ic) {
+            for (; t + CWIN <= tc; t += CWIN) {
+                window_begin<CWIN>(b, s);
+                static_for_up<0, CWIN>([&](auto ic) {
                     const uint32_t z = step<decltype(ic)::value, false>(b, s);
                     *p = z;
                     p += stride;
                     acc_add(a, z);
                 });
-                window_end(b, s);
+                window_end<CWIN>(b, s);
             }
             if (t < tc) {
-                tail_begin(b, s);
+                tail_begin<CWIN>(b, s);
 #pragma unroll 1
                 for (; t < tc; ++t) {
                     const uint32_t z = step<0, false>(b, s);
@@ -354,10 +361,10 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     acc_add(a, z);
                     realign<1>(b, s);
                 }
-                tail_end(b, s);
+                tail_end<CWIN>(b, s);
             }
 #endif
-            store_state<OFF>(state_out, acc_out, G, g, b, s, a);
+            store_state<COFF>(state_out, acc_out, G, g, b, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }
