@@ -16,6 +16,9 @@
 //     scheduler interleaves with the cipher's LOP3s.
 // Only full tiles, whole groups of 32 instances and 32-byte aligned rows come here (mk2_api.cu falls back to
 // grain::gen_rowmajor_kernel otherwise), so there is no ragged code in the loop.
+// Measured (B200, 2^22 instances x 65536 clocks): 10.5-10.6 Tb/s, level with the seven-warp default kernel before
+// that one learnt the in-register transposes (11.4 now) -- lone warps lose to their own latencies what the better
+// store pattern returns.  Opt-in: mk2_set_row_staging(ctx, 4).
 #pragma once
 #include "mk2_grain.cuh"
 
@@ -72,8 +75,11 @@ template <bool LSB, bool DRAIN>
 __device__ __forceinline__ void window(uint32_t (&b)[GW], uint32_t (&s)[GW], HalfSums &hs, uint32_t *zp, const uint32_t *p0,
                                        const uint32_t *p1, uint8_t *dst, uint64_t pitch, bool store)
 {
-    // the drain unit comes first: its loads read blocks this window does not write, and everything after them
-    // (PRMTs, row stores) is free to sink into the cipher's instruction stream
+    // The drain unit comes first (its loads read ring blocks this window does not write).  Its stores are guarded
+    // (`store`: a chunk's first tile has no predecessor), which makes the unit a region of its own in front of the
+    // cipher's instructions.  The branch-free form -- unit and cipher in one basic block -- was measured and is
+    // SLOWER (10.1-10.2 against 10.5-10.6 Tb/s): ptxas then issues all 32 LDS and most of the 64 PRMT before the
+    // first LOP3 of the window (profiles/r02_probe_grain_lone_warps.txt, section 5).
     if constexpr (DRAIN) drain_unit(p0, p1, dst, pitch, store);
     window_begin(b, s);
     uint32_t zz[WIN];
