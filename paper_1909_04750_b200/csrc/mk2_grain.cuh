@@ -122,6 +122,12 @@ constexpr int OFF = MK2_GRAIN_TOP ? WIN : 0;  // where the state sits between tw
 #ifndef MK2_GRAIN_COL_WIN
 #define MK2_GRAIN_COL_WIN 32
 #endif
+#ifndef MK2_GRAIN_ROW_WIN
+#define MK2_GRAIN_ROW_WIN 16
+#endif
+constexpr int RWIN_ = MK2_GRAIN_ROW_WIN;      // window of the default row-major kernel (a divisor of 256, a multiple of 8)
+constexpr int RGW_ = GB + RWIN_;
+constexpr int ROFF_ = MK2_GRAIN_TOP ? RWIN_ : 0;
 constexpr int CWIN = MK2_GRAIN_COL_WIN;
 constexpr int CGW = GB + CWIN;
 constexpr int COFF = MK2_GRAIN_TOP ? CWIN : 0;
@@ -482,9 +488,9 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
         const uint64_t c0 = (uint64_t)k * chunk;
         const uint64_t tc = T - c0 < chunk ? T - c0 : chunk;
         if (g < G) {
-            uint32_t b[GW], s[GW];
+            uint32_t b[RGW_], s[RGW_];
             unsigned long long a;
-            load_state<OFF>(state, acc, G, g, b, s, a);
+            load_state<ROFF_>(state, acc, G, g, b, s, a);
             uint8_t *rows = out + 32 * (g - (uint64_t)chain_base * 32) * pitch + (c0 >> 3);
             const uint64_t nrows = N - 32 * g < 32 ? N - 32 * g : 32;
 #pragma unroll 1
@@ -498,16 +504,16 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                     // full tile: the 8 x 32 bit transposes run in registers on each 8-clock group as it is
                     // produced, so the drain has no load / transpose / store pass over the tile
 #pragma unroll 1
-                    for (; t < nclk; t += WIN) {
-                        window_begin(b, s);
-                        uint32_t zz[WIN];
-                        static_for_up<0, WIN>([&](auto ic) {
+                    for (; t < nclk; t += RWIN_) {
+                        window_begin<RWIN_>(b, s);
+                        uint32_t zz[RWIN_];
+                        static_for_up<0, RWIN_>([&](auto ic) {
                             constexpr int c = decltype(ic)::value;
                             zz[c] = step<c, false>(b, s);
                             hs.add(zz[c]);
                         });
 #pragma unroll
-                        for (int h = 0; h < WIN / 8; ++h) {
+                        for (int h = 0; h < RWIN_ / 8; ++h) {
                             uint32_t z[8];
 #pragma unroll
                             for (int m = 0; m < 8; ++m) z[LSB ? m : 7 - m] = zz[8 * h + m];
@@ -515,8 +521,8 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk) zp[(8 * h + kk) * ts] = z[kk];
                         }
-                        zp += WIN * ts;
-                        window_end(b, s);
+                        zp += RWIN_ * ts;
+                        window_end<RWIN_>(b, s);
                     }
                     hs.fold(a);
                     row_drain<ALIGNED16, TG, TS, LSB, GRAIN_STORE_POLICY, true>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
@@ -524,19 +530,19 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 }
 #endif
 #pragma unroll 1
-                for (; t + WIN <= nclk; t += WIN) {
-                    window_begin(b, s);
-                    static_for_up<0, WIN>([&](auto ic) {
+                for (; t + RWIN_ <= nclk; t += RWIN_) {
+                    window_begin<RWIN_>(b, s);
+                    static_for_up<0, RWIN_>([&](auto ic) {
                         constexpr int c = decltype(ic)::value;
                         const uint32_t z = step<c, false>(b, s);
                         zp[c * ts] = z;
                         hs.add(z);
                     });
-                    zp += WIN * ts;
-                    window_end(b, s);
+                    zp += RWIN_ * ts;
+                    window_end<RWIN_>(b, s);
                 }
                 if (t < nclk) {
-                    tail_begin(b, s);
+                    tail_begin<RWIN_>(b, s);
 #pragma unroll 1
                     for (; t < nclk; ++t) {
                         const uint32_t z = step<0, false>(b, s);
@@ -545,12 +551,12 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                         hs.add(z);
                         realign<1>(b, s);
                     }
-                    tail_end(b, s);
+                    tail_end<RWIN_>(b, s);
                 }
                 hs.fold(a);
                 row_drain<ALIGNED16, TG, TS, LSB, GRAIN_STORE_POLICY>(col, rows + (t0 >> 3), pitch, nclk >> 3, nrows);
             }
-            store_state<OFF>(state_out, acc_out, G, g, b, s, a);
+            store_state<ROFF_>(state_out, acc_out, G, g, b, s, a);
         }
         sched_push(q, slots, mask, progress, chain, k + 1, chunks_per_chain);
     }
