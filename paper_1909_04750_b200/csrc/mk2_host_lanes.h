@@ -97,6 +97,7 @@ public:
         avx2_ = cpu_has_avx2();
         if (const char *v = std::getenv("MK2_LANE_NT")) nt_override_ = std::atoi(v) != 0 ? 1 : 0;
         lanes_override_ = std::getenv("MK2_LANE_ALL") != nullptr;
+        if (const char *v = std::getenv("MK2_LANE_WIDE")) wide_lanes_ = std::max(1, std::atoi(v));
         for (int i = 0; i < nlanes; ++i) lanes_.emplace_back([this, i] { run(i); });
     }
     ~HostCopyLanes()
@@ -121,7 +122,7 @@ public:
         t->nt = avx2_ && (nt_override_ >= 0 ? nt_override_ != 0 : wide);
         // contiguous tiles are at their best with 6-8 lanes (8 MiB non-temporal sub-chunks saturate the memory
         // system; more lanes only compete), pitched row tiles keep gaining up to 16 (profiles/r02_probe_copy_lanes.txt)
-        if (wide && !lanes_override_) t->lanes_wanted = 8;
+        if (wide && !lanes_override_) t->lanes_wanted = wide_lanes_;
         t->rows_per_sub = std::max<size_t>(1, lane_bytes / width);
         t->cols_per_sub = std::min(width, lane_bytes);
         t->sub_bytes = t->rows_per_sub * t->cols_per_sub;
@@ -276,6 +277,7 @@ private:
     bool avx2_ = false;
     int nt_override_ = -1;
     bool lanes_override_ = false;
+    int wide_lanes_ = 8;          // lanes a contiguous tile uses (MK2_LANE_WIDE)
     std::vector<std::thread> lanes_;
     std::mutex m_;
     std::condition_variable cv_, done_;
