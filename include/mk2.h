@@ -257,7 +257,11 @@ int mk2_host_free(void *p);
  * shapes fall back to 0; 10.5-10.6 Tb/s against 10.6-10.7), and column-major
  * on an 80-word circular buffer with no realignment moves (T a multiple of
  * 16; 12.3 Tb/s against 13.8: the 56 KB loop body is instruction-fetch
- * bound).  Modes 3 and 4 on a MICKEY context behave like 0. */
+ * bound); 5 = row-major with EIGHT warps per SM, 28 of a tile's 32 groups in
+ * shared and 4 in tensor memory (whole chains of 1024 instances, full tiles
+ * and 32-byte aligned rows only, other shapes fall back to 0; 10.6-10.8 Tb/s
+ * against 11.4: with eight warps the open row lines no longer fit L2).
+ * Modes 3, 4 and 5 on a MICKEY context behave like 0. */
 int mk2_set_row_staging(mk2_ctx *ctx, int mode);
 /* Tuning knob: mk2_bulk_rowmajor with key/IV arrays AND output on the device can
  * run as one kernel (csrc/mk2_fused.cuh: records -> input words in tensor memory ->

@@ -19,6 +19,7 @@
 #include "mk2_grain.cuh"
 #include "mk2_grain_row64.cuh"
 #include "mk2_grain_ring.cuh"
+#include "mk2_grain_row8.cuh"
 #include "mk2_fused.cuh"
 #include "mk2_coop.cuh"
 #include "mk2_seedgen.cuh"
@@ -312,6 +313,7 @@ struct Plan {
     bool row64;       // Grain row-major: 512-clock tiles, 64 bytes per row and drain (mk2_grain_row64.cuh)
     bool rowl2;       // ... with every warp's tile in L2-resident global scratch
     bool ring;        // Grain row-major: four lone warps per SM, drains pipelined into the next tile (mk2_grain_ring.cuh)
+    bool row8;        // Grain row-major: eight warps per SM, 28 groups of the tile in shared + 4 in tensor memory
 };
 
 Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains, bool ring_ok = false)
@@ -342,6 +344,12 @@ Plan make_plan(const mk2_ctx *ctx, uint64_t T, bool rowmajor, uint64_t chains, b
     if (p.ring) {
         p.block = grain::ring::THREADS;
         p.tg = grain::ring::TILE_GROUPS;
+    }
+    // whole chains only (tcgen05 is warp-collective); plenty of chains, or it has no eighth warp to fill
+    p.row8 = ring_ok && rowmajor && ctx->cipher == 1 && ctx->row_staging == 5 && ctx->N % 1024 == 0 && !ctx->block_user;
+    if (p.row8) {
+        p.block = grain::row8::THREADS;
+        p.tg = 32;
     }
     const uint32_t granule = rowmajor ? 8u * (uint32_t)p.tg : (ctx->cipher == 1 ? (uint32_t)grain::CWIN : 1u);
     auto round_chunk = [&](uint64_t c) {
@@ -451,6 +459,19 @@ int launch_row(mk2_ctx *ctx, uint64_t T, uint8_t *out, uint64_t pitch, uint64_t 
     const Plan p = make_plan(ctx, T, true, nchains, ring_ok);  // chunks are whole staging tiles
     int rc = launch_sched(ctx, p, nchains);
     if (rc) return rc;
+    if (p.row8) {
+        if (ctx->row_lsb)
+            grain::row8::gen_rowmajor_kernel<true><<<p.grid, p.block, grain::row8::SMEM_BYTES, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+        else
+            grain::row8::gen_rowmajor_kernel<false><<<p.grid, p.block, grain::row8::SMEM_BYTES, ctx->stream>>>(
+                ctx->d_state, ctx->d_acc, ctx->d_state, ctx->d_acc, out, pitch, ctx->G, T, p.chunk, p.cpc, ctx->d_queue,
+                ctx->d_slots, ctx->ring - 1, ctx->d_progress, (uint32_t)chain_base);
+        CK(cudaGetLastError());
+        ctx->last_launches++;
+        return MK2_OK;
+    }
     if (p.ring) {
         if (ctx->row_lsb)
             grain::ring::gen_rowmajor_kernel<true><<<p.grid, p.block, grain::ring::SMEM_BYTES, ctx->stream>>>(
@@ -683,6 +704,12 @@ cudaError_t opt_in_row_kernels(int device)
     MK2_OPT_IN_GRAIN(16, 256);
 #undef MK2_OPT_IN_GRAIN
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grain::row8::gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 grain::row8::SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grain::row8::gen_rowmajor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 grain::row8::SMEM_BYTES);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(grain::ring::gen_rowmajor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  grain::ring::SMEM_BYTES);
     if (e == cudaSuccess)
@@ -903,9 +930,10 @@ int mk2_set_chunk_clocks(mk2_ctx *ctx, uint32_t clocks)
 int mk2_set_row_staging(mk2_ctx *ctx, int mode)
 {
     if (!ctx) return MK2_E_ARG;
-    if (mode < 0 || mode > 4)
+    if (mode < 0 || mode > 5)
         return fail(ctx, MK2_E_ARG,
-                    "row staging mode must be 0 (automatic), 1 (shared memory), 2 (tensor memory), 3 (L2 scratch) or 4 (Grain ring)");
+                    "row staging mode must be 0 (automatic), 1 (shared memory), 2 (tensor memory), 3 (L2 scratch), 4 (Grain ring) "
+                    "or 5 (Grain, eight warps)");
     ctx->row_staging = mode;
     return MK2_OK;
 }

@@ -101,7 +101,7 @@ class MickeyGenerator:
     def set_row_staging(self, mode: int):
         """Tuning knob: row-major staging tile in shared memory (1), tensor memory (2) or (Grain only) L2-resident
         global scratch (3); 4 (Grain only) = the lone-warp ring kernel for row-major and the circular-buffer kernel
-        for column-major output (include/mk2.h); 0 = automatic."""
+        for column-major output, 5 (Grain only) = the eight-warp row-major kernel (include/mk2.h); 0 = automatic."""
         self._knobs_touched = True
         self._ck(self._lib.mk2_set_row_staging(self._ctx, int(mode)), "mk2_set_row_staging")
 

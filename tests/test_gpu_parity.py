@@ -984,6 +984,49 @@ def test_grain_rowmajor_ring_kernel(pkg, oracle, N, T, chunk, torch_cuda):
     assert np.array_equal(odd.cpu().numpy()[:, : T // 8], want)
 
 
+@pytest.mark.parametrize("N,T,chunk", [(1024, 256, 0), (1 << 15, 4096 + 512, 1024), (1024 * 37, 2048, 256), (2048, 768, 0),
+                                       (4099, 512, 0), (2048, 1000, 0)])
+def test_grain_rowmajor_eight_warp_kernel(pkg, oracle, N, T, chunk, torch_cuda):
+    """Grain row-major with eight warps per SM (csrc/mk2_grain_row8.cuh, mk2_set_row_staging(ctx, 5)): 28 groups of
+    every 256-clock tile in shared memory, four in tensor memory.  One tile, many tiles, one-tile chunks, both byte
+    orders, resumed calls; shapes it does not take (partial chains, T not a multiple of 256, unaligned rows) fall
+    back to the default kernel.  Same bytes as the oracle, same checksum as the default kernel."""
+    from paper_1909_04750_b200 import grain
+
+    rng = np.random.default_rng(N + T + 1)
+    keys = rng.integers(0, 256, (N, 10), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (N, 8), dtype=np.uint8)
+    want = oracle.grain_bulk_rowmajor(keys, ivs, T)
+    takes = N % 1024 == 0 and T % 256 == 0
+    with grain.GrainGenerator(0) as gen:
+        gen.set_row_staging(5)
+        gen.set_chunk_clocks(chunk)
+        dev = torch_cuda.zeros((N, T // 8), dtype=torch_cuda.uint8, device="cuda")
+        gen.init_material(keys, ivs).generate_rowmajor(T, dev)
+        torch_cuda.cuda.synchronize()
+        if takes:
+            assert gen.last_plan()[0] == 256
+        csum = gen.checksum()
+        lsb = torch_cuda.zeros((N, T // 8), dtype=torch_cuda.uint8, device="cuda")
+        gen.init_material(keys, ivs).generate_rowmajor(T, lsb, bit_order="lsb")
+        two = torch_cuda.zeros((N, T // 8), dtype=torch_cuda.uint8, device="cuda")
+        if T >= 512 and takes:   # resumed: 256 clocks, then the rest
+            gen.init_material(keys, ivs)
+            gen.generate_rowmajor(256, two, byte_offset=0)
+            gen.generate_rowmajor(T - 256, two, byte_offset=32)
+        odd = torch_cuda.zeros((N, T // 8 + 3), dtype=torch_cuda.uint8, device="cuda")   # pitch not a multiple of 32
+        gen.init_material(keys, ivs).generate_rowmajor(T, odd)
+        torch_cuda.cuda.synchronize()
+        gen.set_row_staging(0)
+        gen.init_material(keys, ivs).generate_rowmajor(T)
+        assert gen.checksum() == csum
+    assert np.array_equal(dev.cpu().numpy(), want)
+    assert np.array_equal(lsb.cpu().numpy(), oracle.grain_bulk_rowmajor(keys, ivs, T, "lsb"))
+    if T >= 512 and takes:
+        assert np.array_equal(two.cpu().numpy(), want)
+    assert np.array_equal(odd.cpu().numpy()[:, : T // 8], want)
+
+
 def test_grain_large_sampled(pkg, oracle, torch_cuda):
     """2^20 Grain instances x 4096 bits: sampled groups vs the oracle, layout-independent checksum."""
     from paper_1909_04750_b200 import grain

@@ -21,6 +21,11 @@ with grain.GrainGenerator(0) as gg:
     gg.set_chunk_clocks(768)
     ring = gg.init_material(gk[:1280], gi[:1280]).generate_rowmajor(1024)
     circ = gg.init_material(gk, gi).generate_colmajor(208)
+with grain.GrainGenerator(0) as gg:   # eight-warp kernel: whole chains, three tiles in two chunks
+    gg.set_row_staging(5)
+    gg.set_chunk_clocks(512)
+    row8 = gg.init_material(gk[:1024], gi[:1024]).generate_rowmajor(768)
+assert np.array_equal(row8, orc.grain_bulk_rowmajor(gk[:1024], gi[:1024], 768))
 assert np.array_equal(gcol, orc.grain_bulk_colmajor(gk, gi, 200))
 assert np.array_equal(grow, orc.grain_bulk_rowmajor(gk, gi, 512 + 136))
 assert np.array_equal(glsb, orc.grain_bulk_rowmajor(gk[:1280], gi[:1280], 512, "lsb"))
