@@ -175,6 +175,26 @@ __device__ __forceinline__ void tail_end(uint32_t (&b)[NW], uint32_t (&s)[NW])  
     }
 }
 
+// Checksum accumulator of the Grain loops: HalfSums (two IDP.2A per word) or, with MK2_GRAIN_WIDESUM, ONE 64-bit
+// multiply-add per word by a 1 read from constant memory (IMAD.WIDE; ptxas cannot turn it back into ALU-pipe adds).
+#ifndef MK2_GRAIN_WIDESUM
+#define MK2_GRAIN_WIDESUM 0
+#endif
+struct WideSum {
+    unsigned long long v = 0;
+    __device__ __forceinline__ void add(uint32_t z) { asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(v) : "r"(z), "r"(opaque_one)); }
+    __device__ __forceinline__ void fold(unsigned long long &acc)
+    {
+        acc += v;
+        v = 0;
+    }
+};
+#if MK2_GRAIN_WIDESUM
+using GrainSum = WideSum;
+#else
+using GrainSum = HalfSums;
+#endif
+
 template <int Lo, int Hi, class F>
 __device__ __forceinline__ void static_for_up(F &&f)
 {
@@ -315,7 +335,7 @@ gen_colmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
             while (t < tc) {
                 const uint32_t nseg = tc - t < seg_max ? (uint32_t)(tc - t) : seg_max;
                 uint32_t idx = 0, u = 0;
-                HalfSums hs;
+                GrainSum hs;
 #pragma unroll 1
                 for (; u + CWIN <= nseg; u += CWIN) {
                     window_begin<CWIN>(b, s);
@@ -441,7 +461,7 @@ gen_colmajor_circ_kernel(const uint32_t *state, const unsigned long long *acc, u
             while (t < tc) {
                 const uint32_t nseg = tc - t < seg_max ? (uint32_t)(tc - t) : seg_max;
                 uint32_t idx = 0;
-                HalfSums hs;
+                GrainSum hs;
                 auto seg = [&](auto pc) {
                     static_for_up<0, WIN>([&](auto ic) {
                         const uint32_t z = step<decltype(pc)::value + decltype(ic)::value, false, GB, true>(b, s);
@@ -498,7 +518,7 @@ gen_rowmajor_kernel(const uint32_t *state, const unsigned long long *acc, uint32
                 const int nclk = (tc - t0) >= 8 * TG ? 8 * TG : (int)(tc - t0);  // a multiple of 8
                 uint32_t *zp = col;
                 int t = 0;
-                HalfSums hs;  // checksum on the FMA pipe; a tile is at most 256 words
+                GrainSum hs;  // checksum on the FMA pipe; a tile is at most 256 words
 #if MK2_GRAIN_ROW_FUSED_T
                 if (nclk == 8 * TG) {
                     // full tile: the 8 x 32 bit transposes run in registers on each 8-clock group as it is
